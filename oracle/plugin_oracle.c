@@ -1,0 +1,160 @@
+/*
+ * plugin_oracle.c -- plain, slow, fp64 CPU oracle for the two-stage Gaussian
+ * PLUGIN bandwidth selector of arXiv 1505.02100 (Algorithm 1).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  The
+ * product path (paper_1505_02100_b200/) never links, imports or executes it, and
+ * this file shares no code, header, constant table or helper with the CUDA path.
+ *
+ * What lives here is only the O(n) and O(n^2) arithmetic of Alg. 1, written
+ * literally in binary64 with glibc exp/sqrt (no blocking, fusion, reordering
+ * or fast-math; compile with -O2 -fno-fast-math -ffp-contract=off).  The O(1)
+ * scalar steps (II, III, V, VII, Eq. 4) are written in plain Python in
+ * oracle/oracle.py so they can be read against the paper line by line.
+ *
+ * Parity pins: see tests/test_oracle_pins.py (closed forms for n=1,2, toy data,
+ * 50-digit mpmath brute force for n<=16, Hermite/finite-difference checks of K,
+ * moment identities, the quadrature identity, naive-vs-halved, scale/shift
+ * invariants, the normal-density expectation).  Nothing here is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static const double ORACLE_PI = 3.14159265358979323846264338327950288;
+
+/* Neumaier (improved Kahan-Babuska) compensated summation. */
+typedef struct { double s, c; } neumaier_t;
+static void neumaier_add(neumaier_t* a, double v) {
+  double t = a->s + v;
+  if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v;
+  else                       a->c += (v - t) + a->s;
+  a->s = t;
+}
+static double neumaier_value(const neumaier_t* a) { return a->s + a->c; }
+
+/* Eq. 2: Gaussian kernel K(u) = exp(-u^2/2)/sqrt(2 pi). */
+double oracle_phi(double u) { return exp(-0.5 * u * u) / sqrt(2.0 * ORACLE_PI); }
+
+/* Alg. 1 Step IV: K^(6)(x) = (1/sqrt(2pi)) (x^6 - 15x^4 + 45x^2 - 15) e^{-x^2/2}. */
+double oracle_K6(double x) {
+  double x2 = x * x, x4 = x2 * x2, x6 = x4 * x2;
+  return (x6 - 15.0 * x4 + 45.0 * x2 - 15.0) * exp(-0.5 * x2) / sqrt(2.0 * ORACLE_PI);
+}
+
+/* Alg. 1 Step VI: K^(4)(x) = (1/sqrt(2pi)) (x^4 - 6x^2 + 3) e^{-x^2/2}. */
+double oracle_K4(double x) {
+  double x2 = x * x, x4 = x2 * x2;
+  return (x4 - 6.0 * x2 + 3.0) * exp(-0.5 * x2) / sqrt(2.0 * ORACLE_PI);
+}
+
+/* r in {4, 6}; anything else returns NaN. */
+double oracle_K(int r, double x) {
+  if (r == 6) return oracle_K6(x);
+  if (r == 4) return oracle_K4(x);
+  return NAN;
+}
+
+/*
+ * Alg. 1 Step I on the exact float32 input widened to fp64.
+ * out[0] = sum X_i            (Neumaier)
+ * out[1] = sum X_i^2          (Neumaier)
+ * out[2] = mean = sum X_i / n
+ * out[3] = V_onepass = sum X^2/(n-1) - (sum X)^2/(n(n-1))   -- Step I printed form
+ * out[4] = V_twopass = sum (X_i - mean)^2 / (n-1)          -- its definition (R3)
+ * out[5] = sigma = sqrt(V_twopass)
+ * Returns 0 ok, 1 n<2, 2 non-finite input, 3 V<=0 (degenerate).
+ */
+int oracle_step1(const float* x, int64_t n, double* out) {
+  for (int k = 0; k < 6; ++k) out[k] = NAN;
+  if (n < 2) return 1;
+  neumaier_t s1 = {0, 0}, s2 = {0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    double xi = (double)x[i];
+    if (!isfinite(xi)) return 2;
+    neumaier_add(&s1, xi);
+    neumaier_add(&s2, xi * xi);
+  }
+  double S1 = neumaier_value(&s1), S2 = neumaier_value(&s2);
+  double nd = (double)n;
+  double mean = S1 / nd;
+  double v1 = S2 / (nd - 1.0) - (S1 * S1) / (nd * (nd - 1.0));
+  neumaier_t q = {0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    double dlt = (double)x[i] - mean;
+    neumaier_add(&q, dlt * dlt);
+  }
+  double v2 = neumaier_value(&q) / (nd - 1.0);
+  out[0] = S1; out[1] = S2; out[2] = mean; out[3] = v1; out[4] = v2;
+  if (!(v2 > 0.0)) return 3;
+  out[5] = sqrt(v2);
+  return 0;
+}
+
+/* Eq. 3: Z_i = (X_i - mu) / sigma, fp64. */
+void oracle_zscore(const float* x, int64_t n, double mu, double sigma, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = ((double)x[i] - mu) / sigma;
+}
+
+/* Widen float32 -> fp64 (exact), for the raw-unit path. */
+void oracle_widen(const float* x, int64_t n, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = (double)x[i];
+}
+
+/*
+ * The halved double sum of Eq. 6/7, restricted to rows
+ * i in [i0, i1):  sum_{i0<=i<i1} sum_{j>i} K^(r)((z_i - z_j)/g)
+ * (the division is literal, as in Alg. 1 Steps IV/VI).
+ * Each row is a Neumaier sum over j in index order; rows are then combined in
+ * index order with Neumaier.  Rows are independent, so the OpenMP split over i
+ * does not change the result (bit-identical for any thread count).
+ * out[0], out[1] = Neumaier (sum, compensation) of the row range.
+ */
+void oracle_psi_rows(const double* z, int64_t n, double g, int r, int64_t i0, int64_t i1,
+                     int nthreads, double* out) {
+  if (i0 < 0) i0 = 0;
+  if (i1 > n) i1 = n;
+  out[0] = 0.0; out[1] = 0.0;
+  if (i1 <= i0) return;
+  int64_t m = i1 - i0;
+  double* row = (double*)malloc(sizeof(double) * (size_t)m);
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t k = 0; k < m; ++k) {
+    int64_t i = i0 + k;
+    neumaier_t acc = {0, 0};
+    for (int64_t j = i + 1; j < n; ++j) neumaier_add(&acc, oracle_K(r, (z[i] - z[j]) / g));
+    row[k] = neumaier_value(&acc);
+  }
+  neumaier_t tot = {0, 0};
+  for (int64_t k = 0; k < m; ++k) neumaier_add(&tot, row[k]);
+  free(row);
+  out[0] = tot.s; out[1] = tot.c;
+}
+
+/*
+ * The literal full double sum of Alg. 1 Step IV/VI:
+ * sum_{i=1..n} sum_{j=1..n} K^(r)((z_i - z_j)/g), Neumaier in (i, j) order.
+ * Used for small n to check the halving of Eq. 5-7.
+ */
+double oracle_psi_literal_sum(const double* z, int64_t n, double g, int r) {
+  neumaier_t acc = {0, 0};
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) neumaier_add(&acc, oracle_K(r, (z[i] - z[j]) / g));
+  return neumaier_value(&acc);
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,98 @@
+"""Seeded synthetic inputs shared by the tests, bench.py and the oracle scripts.
+
+This module holds NONE of the method's arithmetic: it only draws samples.
+Recipes follow SURVEY.md App. B.3 exactly (numpy PCG64 ``default_rng(seed)``,
+fixed draw order, draw in float64 then cast to float32).  The paper's own
+datasets (Tables 2-4) are unpublished; these five BASELINE.json
+configurations stand in for them.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+# BASELINE.json "configs", 1-based like the survey.
+CONFIGS = {
+    1: {"n": 1024, "seed": 0, "dist": "N(0,1)"},
+    2: {"n": 16384, "seed": 1, "dist": "0.5*N(-2,0.5^2)+0.5*N(2,1)"},
+    3: {"n": 131072, "seed": 2, "dist": "0.7*U(0,1)+0.3*Exp(rate 2)"},
+    4: {"n": 1048576, "seed": 3, "dist": "N(3,2^2)"},
+    5: {"n": 4194304, "seed": 4, "dist": "5-component Gaussian mixture"},
+}
+
+# SHA-256 of the little-endian float32 bytes.
+SHA256 = {
+    1: "2076690d68521bc28ec2cad06589340ab1f5858ddbfdc701b67428e70a86e143",
+    2: "d8cb9193d43e1159bdb9683c67e53b8c6a617826af3728f311d64f21f9973edf",
+    3: "5d78565c9dbf7ecec14ef8dfa7165317dbe905a381ea3c8a84ecaf099112115f",
+    4: "4155277a9b8793b0867acb277d48f04db85be974ffbbe2269260a5ff73c0f36f",
+    5: "61a92074a14e58f5eb341dd70ff143c6238a095ccf7c7ea60b2d8df2fda5b9b4",
+}
+
+# Paper's toy dataset.
+TOY = np.array([0, 1, 1.1, 1.5, 1.9, 2.8, 2.9, 3.5], dtype=np.float64)
+
+
+def config_data(k: int) -> np.ndarray:
+    """float32 sample of BASELINE config k (1..5)."""
+    if k == 1:
+        r = np.random.default_rng(0)
+        x = r.standard_normal(1024)
+    elif k == 2:
+        r = np.random.default_rng(1)
+        n = 16384
+        c = r.random(n) < 0.5
+        z = r.standard_normal(n)
+        x = np.where(c, -2 + 0.5 * z, 2 + 1.0 * z)
+    elif k == 3:
+        r = np.random.default_rng(2)
+        n = 131072
+        c = r.random(n) < 0.7
+        u = r.random(n)
+        e = r.exponential(0.5, n)
+        x = np.where(c, u, e)
+    elif k == 4:
+        r = np.random.default_rng(3)
+        x = 3 + 2 * r.standard_normal(1048576)
+    elif k == 5:
+        r = np.random.default_rng(4)
+        n = 4194304
+        mu = np.array([-4, -1, 0, 2, 5], dtype=np.float64)
+        sd = np.array([0.3, 1, 0.5, 0.8, 2], dtype=np.float64)
+        c = r.integers(0, 5, n)
+        z = r.standard_normal(n)
+        x = mu[c] + sd[c] * z
+    else:
+        raise ValueError(f"unknown config {k}")
+    return np.ascontiguousarray(x.astype(np.float32))
+
+
+def sha256_f32(x: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(x, dtype="<f4").tobytes()).hexdigest()
+
+
+def normal(n: int, seed: int, mean: float = 0.0, sd: float = 1.0) -> np.ndarray:
+    r = np.random.default_rng(seed)
+    return (mean + sd * r.standard_normal(n)).astype(np.float32)
+
+
+def mixture(n: int, seed: int) -> np.ndarray:
+    """3-component Gaussian mixture (SPEC.md S:325-style test data)."""
+    r = np.random.default_rng(seed)
+    mu = np.array([-3.0, 0.0, 2.5])
+    sd = np.array([0.5, 1.0, 0.3])
+    c = r.integers(0, 3, n)
+    return (mu[c] + sd[c] * r.standard_normal(n)).astype(np.float32)
+
+
+def ties(n: int, seed: int, levels: int = 37) -> np.ndarray:
+    """Heavy duplicates: N(0,1) rounded onto a coarse grid (many u = 0 pairs)."""
+    r = np.random.default_rng(seed)
+    return (np.round(r.standard_normal(n) * levels / 6.0) * (6.0 / levels)).astype(np.float32)
+
+
+def offset(n: int, seed: int, base: float = 1.0e6) -> np.ndarray:
+    """Large location offset: base + N(0,1) (stresses difference-first evaluation)."""
+    r = np.random.default_rng(seed)
+    return (base + r.standard_normal(n)).astype(np.float32)
