@@ -1,0 +1,147 @@
+/*
+ * plugin.h -- C ABI of libplugin.so, the B200 (sm_100a) hot path of the
+ * two-stage Gaussian PLUGIN bandwidth selector of arXiv 1505.02100
+ * (Algorithm 1).
+ *
+ * Problem statement: "data set X containing n elements" -> "value h
+ * represents the optimal bandwidth for kernel density estimation".  The O(n^2)
+ * part is Steps IV and VI, the pairwise functionals
+ *     Psi_r(g) = (n^2 g^(r+1))^-1 sum_i sum_j K^(r)((X_i - X_j)/g),  r in {6, 4},
+ * evaluated with the symmetry of Eq. 5-7; everything else is O(n)
+ * (Step I) or O(1) (Steps II, III, V, VII, Eq. 4).
+ *
+ * Conventions for every entry point
+ *  - Pointers named d_* are CUDA device pointers on the current device; h_* are
+ *    host pointers.  `stream` is a cudaStream_t passed as void* (0 = legacy stream).
+ *  - The caller owns all memory: the input sample, the result, the workspace.
+ *    The library allocates nothing, keeps no global mutable state except a
+ *    thread-local error string, and never synchronises the stream except in the
+ *    *_sync / *_host calls; the asynchronous calls are CUDA-graph capturable.
+ *  - Input X is float32, contiguous, not modified.  Workspace: at least
+ *    plugin_workspace_bytes(n) bytes, 256-byte aligned, no initialisation needed;
+ *    two calls may run concurrently only with distinct workspaces.
+ *  - Return value (plugin_status): immediate errors only -- PLUGIN_E_INVALID for
+ *    bad arguments (null pointer, n out of range, r not in {4,6}, g not finite
+ *    and > 0, workspace too small, rank/world inconsistent) and PLUGIN_E_CUDA for
+ *    a launch failure.  Data-dependent errors (non-finite sample, zero variance,
+ *    psi6 >= 0, psi4 <= 0) are written by the device into plugin_result.status;
+ *    fields that were not reached are NaN.  plugin_last_error() describes the
+ *    last non-OK return of the calling thread.  Nothing aborts or throws.
+ *  - Units: fields without suffix are in the data's own units (Eq. 4 applied);
+ *    *_z fields are the paper's z-score units (Eq. 3).
+ */
+#ifndef PAPER_1505_02100_PLUGIN_H
+#define PAPER_1505_02100_PLUGIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PLUGIN_OK = 0,
+  PLUGIN_E_INVALID = 1,     /* bad argument (immediate)                                  */
+  PLUGIN_E_NONFINITE = 2,   /* NaN/Inf in X (device status)                              */
+  PLUGIN_E_DEGENERATE = 3,  /* Step I variance V <= 0, e.g. all X equal (device status)  */
+  PLUGIN_E_DOMAIN = 4,      /* psi6 >= 0 (Step V) or psi4 <= 0 (Step VII) (device)       */
+  PLUGIN_E_CUDA = 5         /* a CUDA launch / copy failed (immediate)                   */
+} plugin_status;
+
+/* Written by the device.  Layout is part of the ABI (int32,int32,int64, then doubles). */
+typedef struct {
+  int32_t status;     /* plugin_status of the data-dependent checks                          */
+  int32_t reserved;
+  int64_t n;
+  double mean;        /* Step I: sample mean                                       */
+  double var;         /* Step I: V = sum X^2/(n-1) - (sum X)^2/(n(n-1)) (evaluated shifted)   */
+  double sigma;       /* Step I: sigma = sqrt(V)                                             */
+  double psi8_ns;     /* Step II: 105/(32 sqrt(pi) sigma^9)                        */
+  double g1;          /* Step III                                                  */
+  double psi6;        /* Step IV at g1                                            */
+  double g2;          /* Step V                                                  */
+  double psi4;        /* Step VI at g2                                           */
+  double h;           /* Step VII with Eq. 4: h = h_z * sigma         */
+  double g1_z, psi6_z, g2_z, psi4_z, h_z;   /* the same in z-score units (sigma_z = 1)       */
+  double S6, S4;      /* sum_i sum_j P_r(t_ij) 2^(-t_ij log2(e)/2), t = ((X_i-X_j)/g)^2: the
+                         full double sums of Steps IV/VI divided by phi(0) (diagnostics)     */
+} plugin_result;
+
+/* Fixed-point partial of a psi pass (multi-GPU building block):
+ * the sum over this rank's pairs as a signed 128-bit integer in units of 2^-64,
+ * stored as four 32-bit limbs held in int64 (limb k = bits [32k, 32k+32), limb 3
+ * signed).  Integer addition is associative, so an NCCL allreduce(SUM, int64) of
+ * these 4 words over any number of ranks gives the bit-identical total. */
+typedef struct { int64_t limb[4]; } plugin_fx128;
+
+/* Bytes of workspace needed for n samples (covers every call below). */
+size_t plugin_workspace_bytes(int64_t n);
+
+/*
+ * plugin_h: the whole Algorithm 1 on the device, asynchronously on `stream`.
+ *   d_x   : device float32[n], n >= 2 (Step I divides by n-1; reading s9 of DESIGN.md)
+ *   d_out : device plugin_result, written when the stream reaches the end of the call
+ * Launches: Step I reduction, a sort of X into the workspace (summation order only),
+ * the Step IV pass, its finalize (psi6, g2), the Step VI pass, its finalize (psi4, h).
+ */
+plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
+                       void* d_ws, size_t ws_bytes, void* stream);
+
+/* Same as plugin_h (device result kept in the workspace), then synchronises `stream`,
+ * copies the result to *h_out and returns its data status (PLUGIN_OK or one of
+ * E_NONFINITE/E_DEGENERATE/E_DOMAIN). */
+plugin_status plugin_h_sync(const float* d_x, int64_t n, plugin_result* h_out,
+                            void* d_ws, size_t ws_bytes, void* stream);
+
+/* End to end from HOST memory: copies h_x (float32[n], ideally pinned) into the
+ * workspace, runs plugin_h, copies the result back to *h_out, synchronises and
+ * returns the data status.  Needs plugin_host_workspace_bytes(n) bytes of workspace
+ * (= plugin_workspace_bytes(n) plus room for the copy of X). */
+size_t plugin_host_workspace_bytes(int64_t n);
+plugin_status plugin_h_host(const float* h_x, int64_t n, plugin_result* h_out,
+                            void* d_ws, size_t ws_bytes, void* stream);
+
+/*
+ * psi_r: Psi_r(g) of Steps IV/VI for a given bandwidth g (data units), r in {4,6}:
+ *   Psi_r(g) = (n^2 g^(r+1))^-1 sum_{i,j} K^(r)((x_i - x_j)/g), diagonal included,
+ * evaluated as 2 sum_{i<j} + n K^(r)(0) (Eq. 6/7).  n >= 1, g finite > 0.
+ * *d_psi (device double) is written; a non-finite sample makes it NaN.
+ */
+plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- multi-GPU building blocks (one process per GPU; the caller allreduces) ---- */
+
+/* Step I..III on this rank's full copy of X: fills mean, var, sigma, psi8_ns, g1(_z),
+ * status in d_out and prepares the workspace (sorted X) for the psi shards. */
+plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
+                           void* d_ws, size_t ws_bytes, void* stream);
+
+/* One rank's share of a psi pass: the tiles [w*rank/world, w*(rank+1)/world) of the
+ * pair triangle (w = plugin_num_tiles(n)), at the bandwidth of d_out (g1 for r=6,
+ * g2 for r=4), written as an unnormalised fixed-point sum to *d_partial.
+ * Requires plugin_step1 (and plugin_after_psi6 for r=4) on the same workspace. */
+plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_result* d_out,
+                          plugin_fx128* d_partial, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Finalize a pass from the all-reduced fixed-point total: psi6 and g2 (r=6), or
+ * psi4 and h (r=4), into d_out (data status E_DOMAIN if the sign check fails). */
+plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
+plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
+
+/* Number of equal-work tiles of the pair triangle for n, and the tile range
+ * [begin, end) that `rank` of `world` owns (what psi_r_shard processes). */
+int64_t plugin_num_tiles(int64_t n);
+void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
+
+/* Text of the last non-OK return on this thread ("" if none).  Static storage. */
+const char* plugin_last_error(void);
+
+/* Library / build identification, e.g. "libplugin sm_100a tile=2048". */
+const char* plugin_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_1505_02100_PLUGIN_H */

@@ -1,0 +1,248 @@
+// abi.cu -- the extern "C" boundary of libplugin.so (declared in include/plugin.h).
+// Host-side argument checks, workspace layout and launch sequencing only; every step
+// of the method runs in the kernels of scalar.cu / sort.cu / psi.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace plg {
+
+static thread_local char g_err[512] = "";
+
+static plugin_status fail(plugin_status st, const char* fmt, const char* a = "", long long b = 0) {
+  snprintf(g_err, sizeof(g_err), fmt, a, b);
+  return st;
+}
+static plugin_status cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return PLUGIN_E_CUDA;
+}
+
+constexpr int64_t kMaxN = (int64_t)1 << 31;  // keeps tile indices and sort offsets in 32 bits
+
+Layout layout(int64_t n) {
+  Layout L;
+  size_t off = 0;
+  L.ctrl = off;
+  off = align_up(off + sizeof(Ctrl), 256);
+  L.step1 = off;
+  off = align_up(off + sizeof(double) * 2 * kStep1Blocks, 256);
+  L.xs = off;
+  off = align_up(off + sizeof(float) * (size_t)(n > 0 ? n : 1), 256);
+  L.tmp = off;
+  off = align_up(off + sizeof(unsigned int) * (size_t)(n > 0 ? n : 1), 256);
+  L.sort_blocks = (n + kSortTile - 1) / kSortTile;
+  if (L.sort_blocks < 1) L.sort_blocks = 1;
+  L.hist = off;
+  off = align_up(off + sizeof(unsigned int) * 256 * (size_t)L.sort_blocks, 256);
+  L.result = off;
+  off = align_up(off + sizeof(plugin_result), 256);
+  L.total = off;
+  return L;
+}
+
+struct WS {
+  Layout L;
+  Ctrl* ctrl;
+  double* step1;
+  float* xs;
+  unsigned int* tmp;
+  unsigned int* hist;
+};
+
+static plugin_status get_ws(void* d_ws, size_t ws_bytes, int64_t n, WS& w) {
+  w.L = layout(n);
+  if (!d_ws) return fail(PLUGIN_E_INVALID, "workspace pointer is null%s", "");
+  if ((reinterpret_cast<uintptr_t>(d_ws) & 255u) != 0) return fail(PLUGIN_E_INVALID, "workspace not 256-byte aligned%s", "");
+  if (ws_bytes < w.L.total)
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)w.L.total);
+  char* b = static_cast<char*>(d_ws);
+  w.ctrl = reinterpret_cast<Ctrl*>(b + w.L.ctrl);
+  w.step1 = reinterpret_cast<double*>(b + w.L.step1);
+  w.xs = reinterpret_cast<float*>(b + w.L.xs);
+  w.tmp = reinterpret_cast<unsigned int*>(b + w.L.tmp);
+  w.hist = reinterpret_cast<unsigned int*>(b + w.L.hist);
+  return PLUGIN_OK;
+}
+
+static plugin_status check_n(int64_t n, int64_t nmin) {
+  if (n < nmin || n > kMaxN) return fail(PLUGIN_E_INVALID, "n out of range%s (n=%lld)", "", (long long)n);
+  return PLUGIN_OK;
+}
+
+// Step I..III + sort into the workspace
+static plugin_status run_step1(const float* d_x, int64_t n, plugin_result* d_out, WS& w, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
+  if ((e = launch_init_result(d_out, n, s)) != cudaSuccess) return cuda_fail(e, "init_result");
+  // sort first: Step I then reads the sorted copy, so every result is a function of the
+  // multiset of X only (bit-identical under any permutation of the input)
+  if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
+  if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, d_out, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  return PLUGIN_OK;
+}
+
+}  // namespace plg
+
+using namespace plg;
+
+extern "C" {
+
+size_t plugin_workspace_bytes(int64_t n) { return layout(n).total; }
+
+size_t plugin_host_workspace_bytes(int64_t n) {
+  return layout(n).total + align_up(sizeof(float) * (size_t)(n > 0 ? n : 1), 256);
+}
+
+int64_t plugin_num_tiles(int64_t n) { return n > 0 ? psi_tiles(n) : 0; }
+
+void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end) {
+  int64_t w = plugin_num_tiles(n);
+  if (world < 1 || rank < 0 || rank >= world) {
+    if (begin) *begin = 0;
+    if (end) *end = 0;
+    return;
+  }
+  // equal-work tiles: contiguous, balanced to within one tile
+  if (begin) *begin = (w * rank) / world;
+  if (end) *end = (w * (rank + 1)) / world;
+}
+
+const char* plugin_last_error(void) { return g_err; }
+
+const char* plugin_version(void) { return "libplugin 0.1 sm_100a (psi: f32x2 + MUFU.EX2, dithered; fx128 accumulation)"; }
+
+plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
+  const int64_t tiles = psi_tiles(n);
+  cudaError_t e;
+  if ((e = launch_psi(w.xs, n, 6, 0, 0.0, d_out, w.ctrl, 0, 0, tiles, s)) != cudaSuccess) return cuda_fail(e, "psi6");
+  if ((e = launch_finalize(0, w.ctrl, 0, nullptr, d_out, n, 0.0, 6, nullptr, nullptr, s)) != cudaSuccess)
+    return cuda_fail(e, "finalize psi6");
+  if ((e = launch_psi(w.xs, n, 4, 1, 0.0, d_out, w.ctrl, 1, 0, tiles, s)) != cudaSuccess) return cuda_fail(e, "psi4");
+  if ((e = launch_finalize(1, w.ctrl, 1, nullptr, d_out, n, 0.0, 4, nullptr, nullptr, s)) != cudaSuccess)
+    return cuda_fail(e, "finalize psi4");
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_h_sync(const float* d_x, int64_t n, plugin_result* h_out, void* d_ws, size_t ws_bytes,
+                            void* stream) {
+  if (!h_out) return fail(PLUGIN_E_INVALID, "null result pointer%s");
+  WS w;
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  plugin_result* d_out = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = plugin_h(d_x, n, d_out, d_ws, ws_bytes, stream)) != PLUGIN_OK) return st;
+  cudaError_t e = cudaMemcpyAsync(h_out, d_out, sizeof(plugin_result), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "copy result");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+  return static_cast<plugin_status>(h_out->status);
+}
+
+plugin_status plugin_h_host(const float* h_x, int64_t n, plugin_result* h_out, void* d_ws, size_t ws_bytes,
+                            void* stream) {
+  g_err[0] = 0;
+  if (!h_x || !h_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  if (ws_bytes < plugin_host_workspace_bytes(n))
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)plugin_host_workspace_bytes(n));
+  const Layout L = layout(n);
+  const size_t base = L.total;
+  char* b = static_cast<char*>(d_ws);
+  float* d_x = reinterpret_cast<float*>(b + base);
+  plugin_result* d_out = reinterpret_cast<plugin_result*>(b + L.result);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(d_x, h_x, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "copy X to device");
+  if ((st = plugin_h(d_x, n, d_out, d_ws, base, stream)) != PLUGIN_OK) return st;
+  if ((e = cudaMemcpyAsync(h_out, d_out, sizeof(plugin_result), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "copy result");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+  return static_cast<plugin_status>(h_out->status);
+}
+
+plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi, void* d_ws, size_t ws_bytes,
+                    void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_psi) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  if (r != 4 && r != 6) return fail(PLUGIN_E_INVALID, "r must be 4 or 6%s (r=%lld)", "", r);
+  if (!(std::isfinite(g) && g > 0.0)) return fail(PLUGIN_E_INVALID, "g must be finite and > 0%s");
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
+  if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
+  // Step I reduction only for its non-finite flag (a NaN/Inf sample makes Psi NaN)
+  plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
+  if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  if ((e = launch_psi(w.xs, n, r, 2, g, nullptr, w.ctrl, 1, 0, psi_tiles(n), s)) != cudaSuccess)
+    return cuda_fail(e, "psi");
+  if ((e = launch_finalize(2, w.ctrl, 1, nullptr, nullptr, n, g, r, d_psi, nullptr, s)) != cudaSuccess)
+    return cuda_fail(e, "finalize");
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes,
+                           void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  return run_step1(d_x, n, d_out, w, static_cast<cudaStream_t>(stream));
+}
+
+plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_result* d_out,
+                          plugin_fx128* d_partial, void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_out || !d_partial) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  if (r != 4 && r != 6) return fail(PLUGIN_E_INVALID, "r must be 4 or 6%s (r=%lld)", "", r);
+  if (world < 1 || rank < 0 || rank >= world) return fail(PLUGIN_E_INVALID, "bad rank/world%s");
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  int64_t tb, te;
+  plugin_shard_tiles(n, rank, world, &tb, &te);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int slot = (r == 6) ? 0 : 1;
+  cudaError_t e = launch_psi(w.xs, n, r, r == 6 ? 0 : 1, 0.0, d_out, w.ctrl, slot, tb, te, s);
+  if (e != cudaSuccess) return cuda_fail(e, "psi shard");
+  if ((e = launch_finalize(3, w.ctrl, slot, nullptr, nullptr, n, 0.0, r, nullptr, d_partial, s)) != cudaSuccess)
+    return cuda_fail(e, "export partial");
+  return PLUGIN_OK;
+}
+
+static plugin_status after(int what, const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
+  g_err[0] = 0;
+  if (!d_total || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  cudaError_t e = launch_finalize(what, nullptr, 0, d_total, d_out, 0, 0.0, what == 0 ? 6 : 4, nullptr, nullptr,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "finalize");
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
+  return after(0, d_total, d_out, stream);
+}
+plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
+  return after(1, d_total, d_out, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// common.cuh -- shared device/host pieces of libplugin.so (workspace layout,
+// fixed-point accumulator, launch declarations).  Product code: nothing here is
+// shared with oracle/.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/plugin.h"
+
+namespace plg {
+
+// ---- constants of Algorithm 1, fp64 -----------------------
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr double kInvSqrt2Pi = 0.398942280401432677939946059934381868;  // phi(0), Eq. 2
+constexpr double kK6at0 = -15.0 * kInvSqrt2Pi;   // Step III  K^6(0) = -15/sqrt(2 pi)
+constexpr double kK4at0 = 3.0 * kInvSqrt2Pi;     // Step V  K^4(0) =  3/sqrt(2 pi)
+constexpr double kRK = 0.282094791773878143474039725780386293;  // Step VII R(K) = 1/(2 sqrt(pi))
+constexpr double kMu2 = 1.0;                                    // mu_2(K) = 1
+
+// ---- tiling --------------------------------------------------------------------
+constexpr int kPsiThreads = 256;   // threads per CTA of the psi pass
+constexpr int kSortTile = 4096;    // keys per CTA in the radix sort
+constexpr int kSortThreads = 256;
+constexpr int kStep1Blocks = 592;  // 4 x 148: fixed grid so Step I is deterministic
+
+// rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
+int psi_rows_per_thread(int64_t n);
+inline int64_t psi_tile_edge(int64_t n) { return (int64_t)kPsiThreads * psi_rows_per_thread(n); }
+inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
+inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
+
+// ---- signed 128-bit fixed point, value = hi + lo * 2^-64 ------------------------
+struct Fx128 { unsigned long long lo; long long hi; };
+
+// ---- workspace layout ----------------------------------------------------------
+struct Ctrl {                       // zeroed at the start of every API call
+  Fx128 acc[2];                     // psi accumulators (slot 0: r=6, slot 1: r=4 / psi_r)
+  unsigned int tile_counter[2];     // dynamic tile scheduler per slot
+  unsigned int step1_done;          // last-block-done counter of Step I
+  int nonfinite;                    // set if any X is NaN/Inf
+  unsigned int pad[58];
+};
+static_assert(sizeof(Ctrl) <= 512, "ctrl block");
+
+struct Layout {
+  size_t ctrl, step1, xs, tmp, hist, result, total;
+  int64_t sort_blocks;
+};
+Layout layout(int64_t n);
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- launchers (each returns cudaGetLastError()) ----------------------------------
+cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials, plugin_result* out,
+                         cudaStream_t s);
+cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
+                        int64_t nblocks, cudaStream_t s);
+// mode: 0 = plugin pass r=6 (g from out->g1), 1 = plugin pass r=4 (g from out->g2),
+//       2 = psi_r with host g
+cudaError_t launch_psi(const float* xs, int64_t n, int r, int mode, double g_host, const plugin_result* out,
+                       Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, cudaStream_t s);
+// what: 0 = plugin r=6 finalize, 1 = plugin r=4 finalize, 2 = psi_r -> d_psi, 3 = export limbs
+cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* total, plugin_result* out,
+                            int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
+                            cudaStream_t s);
+cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
+
+}  // namespace plg

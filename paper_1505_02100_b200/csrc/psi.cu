@@ -1,0 +1,322 @@
+// psi.cu -- the O(n^2) hot path: Steps IV and VI of Algorithm 1
+// evaluated with the symmetry of Eq. 5-7 on sm_100a.
+//
+// Work unit: a T x T tile (T = 256 R) of the upper block triangle of the sorted sample.
+// Off-diagonal tiles count each pair once with weight 2; diagonal tiles are evaluated as
+// full squares (both orders plus the exact i = j terms) with weight 1, which is
+// 2 sum_{i<j} + n K(0) of Eq. 6/7 without a mask.  Persistent CTAs pull tiles from an
+// atomic counter.  Each thread keeps R rows i in registers and streams the tile's j values
+// from shared memory (one LDS.128 broadcast per 4 j); two pairs go through each packed
+// f32x2 instruction:
+//     d = x_j - x_i (difference first, raw fp32)   u = d*s (s = fp32(1/g))   t = u*u
+//     a = t*c + p_i   (c = fp32(-log2(e)/2), p_i in (-2, -1] a per-row phase)   e = ex2.approx(a)
+//     P6 = ((t - 15) t + 45) t - 15   |   P4 = (t - 6) t + 3      (exact integer coefficients)
+//     acc += P * e
+// i.e. 8 (r=6) / 7 (r=4) FP32 lane-ops and 1 MUFU.EX2 per pair.  Numerics:
+// the per-row phase p_i = -1 - frac(i * 0.618...) (24 random bits, a Weyl sequence)
+// dithers the SFU exp argument so the table-pattern bias of MUFU.EX2 averages to a
+// constant, and keeps |a| >= 1 (no input truncation inside MUFU); it is undone by scaling
+// each row's fp64 sum by 2^(-p_i) in fp64.  The per-row scale s_i = s + k_i ulp(s),
+// k_i in [-7, 7], decorrelates the fp32 rounding of u and t across rows (matters for
+// discretised samples with few distinct differences); it is a zero-mean dilation of
+// <= 1e-6 whose effect is second order.
+// fp32 accumulators hold 16 terms per lane, then go to per-row fp64; each tile's fp64
+// total is added as a 128-bit fixed-point integer, so the result does not depend on
+// tile scheduling, grid size or GPU count.
+#include "common.cuh"
+
+namespace plg {
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2(float a) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+
+// packed constants {v, v}
+#define PK(v) ((((u64)__float_as_uint(v)) << 32) | (u64)__float_as_uint(v))
+
+// per-row dither: phase p_i in (-2, -1] (exact fp32, 24 random bits) and scale offset k_i in [-7, 7]
+__device__ __forceinline__ unsigned int row_hash(int64_t i) { return (unsigned int)i * 2654435769u; }
+__device__ __forceinline__ float row_phase(int64_t i) {
+  return -1.0f - (float)(row_hash(i) >> 8) * (1.0f / 16777216.0f);
+}
+__device__ __forceinline__ int row_scale_offset(int64_t i) {
+  unsigned int h = ((unsigned int)i * 0x85EBCA6Bu) ^ 0x9E3779B9u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  return (int)(((h >> 16) * 15u) >> 16) - 7;
+}
+
+template <int ORDER, bool MASK>
+__device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, bool m0 = true, bool m1 = true) {
+  const u64 c2 = 0xBF38AA3BBF38AA3Bull;  // {fp32(-log2(e)/2)} x 2 = -0.72134752f
+  u64 d = sub2(xj, xi);
+  u64 u = mul2(d, s2);
+  u64 t = mul2(u, u);
+  u64 a = fma2(t, c2, ph);
+  float a0, a1;
+  upk2(a, a0, a1);
+  float e0 = ex2(a0), e1 = ex2(a1);
+  if (MASK) {
+    e0 = m0 ? e0 : 0.f;
+    e1 = m1 ? e1 : 0.f;
+  }
+  u64 e = pk2(e0, e1);
+  u64 p;
+  if (ORDER == 6) {
+    p = add2(t, 0xC1700000C1700000ull);      // t - 15
+    p = fma2(p, t, 0x4234000042340000ull);   // (t - 15) t + 45
+    p = fma2(p, t, 0xC1700000C1700000ull);   // ((t - 15) t + 45) t - 15
+  } else {
+    p = add2(t, 0xC0C00000C0C00000ull);      // t - 6
+    p = fma2(p, t, 0x4040000040400000ull);   // (t - 6) t + 3
+  }
+  acc = fma2(p, e, acc);
+}
+
+// float -> double on the integer (ALU) pipe.  cvt.f64.f32 (F2F) issues on the XU pipe,
+// which MUFU.EX2 saturates; fp32 denormals and zero map to +-0, Inf/NaN are not expected
+// (non-finite samples are rejected before the pass).
+__device__ __forceinline__ double f32_to_f64_alu(float f) {
+  const unsigned int b = __float_as_uint(f);
+  const unsigned int mag = b & 0x7fffffffu;
+  unsigned int hi = ((mag >> 3) + 0x38000000u) | (b & 0x80000000u);
+  unsigned int lo = b << 29;
+  const bool tiny = mag < 0x00800000u;
+  hi = tiny ? (b & 0x80000000u) : hi;
+  lo = tiny ? 0u : lo;
+  return __hiloint2double((int)hi, (int)lo);
+}
+
+__device__ __forceinline__ Fx128 fx_from_double(double x) {
+  Fx128 r;
+  double fl = floor(x);
+  r.hi = (long long)fl;
+  double fr = x - fl;  // exact, in [0, 1)
+  r.lo = __double2ull_rn(fr * 18446744073709551616.0);
+  return r;
+}
+__device__ __forceinline__ void fx_add(Fx128& a, Fx128 b) {
+  unsigned long long lo = a.lo + b.lo;
+  a.hi += b.hi + (lo < a.lo ? 1 : 0);
+  a.lo = lo;
+}
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, int64_t& bj) {
+  // row-major upper triangle incl. diagonal: row b starts at off(b) = b*nb - b(b-1)/2
+  double A = 2.0 * (double)nb + 1.0;
+  int64_t b = (int64_t)((A - sqrt(A * A - 8.0 * (double)t)) * 0.5);
+  if (b < 0) b = 0;
+  if (b > nb - 1) b = nb - 1;
+  while (b > 0 && b * nb - b * (b - 1) / 2 > t) --b;
+  while (b + 1 < nb && (b + 1) * nb - (b + 1) * b / 2 <= t) ++b;
+  bi = b;
+  bj = b + (t - (b * nb - b * (b - 1) / 2));
+}
+
+template <int R, int ORDER>
+__global__ void __launch_bounds__(kPsiThreads, 2)
+psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, const plugin_result* __restrict__ out,
+           Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
+  constexpr int T = kPsiThreads * R;
+  constexpr int CH = 64;  // j per fp32 chunk (32 per packed lane) before the fp64 flush
+  __shared__ __align__(16) float sx[T];
+  __shared__ double red[kPsiThreads / 32];
+  __shared__ long long s_tile;
+
+  double g = g_host;
+  if (mode == 0 || mode == 1) {
+    if (out->status != PLUGIN_OK) return;
+    g = (mode == 0) ? out->g1 : out->g2;
+  }
+  const float s = __double2float_rn(1.0 / g);
+  const int64_t nb = (n + T - 1) / T;
+  const float xpad = __ldg(xs + n - 1);
+  Fx128 cta_acc = {0ull, 0ll};
+  const int tid = threadIdx.x;
+
+  for (;;) {
+    if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    if (t >= tile_end) break;
+    int64_t bi, bj;
+    tile_coords(t, nb, bi, bj);
+    const int64_t i0 = bi * T, j0 = bj * T;
+    const int jcount = (int)((n - j0) < T ? (n - j0) : T);
+    // stage the tile's j values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
+    if (jcount == T) {
+      const float4* src = reinterpret_cast<const float4*>(xs + j0);
+      float4* dst = reinterpret_cast<float4*>(sx);
+#pragma unroll
+      for (int q = 0; q < T / 4 / kPsiThreads; ++q) dst[q * kPsiThreads + tid] = __ldg(src + q * kPsiThreads + tid);
+      if (T / 4 < kPsiThreads && tid < T / 4) dst[tid] = __ldg(src + tid);
+    } else {
+      for (int q = tid; q < T; q += kPsiThreads) sx[q] = (q < jcount) ? __ldg(xs + j0 + q) : xpad;
+    }
+    u64 xi[R], ph[R], s2[R];
+    double drow[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = i0 + k * kPsiThreads + tid;
+      const float v = (i < n) ? __ldg(xs + i) : xpad;
+      xi[k] = pk2(v, v);
+      const float p = row_phase(i);
+      ph[k] = pk2(p, p);
+      const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+      s2[k] = pk2(si, si);
+      drow[k] = 0.0;
+    }
+    __syncthreads();
+    const float4* sx4 = reinterpret_cast<const float4*>(sx);
+    const int full = jcount / CH;
+    for (int c = 0; c < full; ++c) {
+      u64 acc[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = 0ull;
+#pragma unroll 2
+      for (int q = 0; q < CH / 4; ++q) {
+        const float4 v = sx4[c * (CH / 4) + q];
+        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          pair2<ORDER, false>(j01, xi[k], s2[k], ph[k], acc[k]);
+          pair2<ORDER, false>(j23, xi[k], s2[k], ph[k], acc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        float a0, a1;
+        upk2(acc[k], a0, a1);
+        drow[k] += f32_to_f64_alu(a0 + a1);
+      }
+    }
+    if (full * CH < jcount) {  // ragged last chunk of the last column tile
+      u64 acc[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = 0ull;
+      const int jb = full * CH;
+      for (int q = 0; q < CH / 4; ++q) {
+        const float4 v = sx4[full * (CH / 4) + q];
+        const int j = jb + 4 * q;
+        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          pair2<ORDER, true>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
+          pair2<ORDER, true>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        float a0, a1;
+        upk2(acc[k], a0, a1);
+        drow[k] += f32_to_f64_alu(a0 + a1);
+      }
+    }
+    // undo the dither per row, drop padding rows, weight the tile
+    double tsum = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = i0 + k * kPsiThreads + tid;
+      const double comp = exp2(-(double)row_phase(i));
+      if (i < n) tsum = fma(drow[k], comp, tsum);
+    }
+    const double w = (bi == bj) ? 1.0 : 2.0;
+    tsum *= w;
+    for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+    if ((tid & 31) == 0) red[tid >> 5] = tsum;
+    __syncthreads();
+    if (tid == 0) {
+      double tt = 0.0;
+#pragma unroll
+      for (int k = 0; k < kPsiThreads / 32; ++k) tt += red[k];
+      fx_add(cta_acc, fx_from_double(tt));
+    }
+    // next iteration's first __syncthreads orders the smem reuse
+  }
+  if (tid == 0 && (cta_acc.lo != 0ull || cta_acc.hi != 0ll)) {
+    unsigned long long* g_lo = &ctrl->acc[slot].lo;
+    unsigned long long* g_hi = reinterpret_cast<unsigned long long*>(&ctrl->acc[slot].hi);
+    unsigned long long old = atomicAdd(g_lo, cta_acc.lo);
+    unsigned long long carry = (old + cta_acc.lo < old) ? 1ull : 0ull;
+    atomicAdd(g_hi, (unsigned long long)cta_acc.hi + carry);
+  }
+}
+
+int psi_rows_per_thread(int64_t n) {
+  // largest R in {8,4,2} whose tile count keeps >= ~28 tiles per resident CTA (296 on 148 SMs)
+  const int cand[3] = {8, 4, 2};
+  for (int c : cand) {
+    int64_t T = (int64_t)kPsiThreads * c, nb = (n + T - 1) / T;
+    if (nb * (nb + 1) / 2 >= 8192) return c;
+  }
+  return 1;
+}
+
+template <int R, int ORDER>
+static cudaError_t launch_t(const float* xs, int64_t n, int mode, double g, const plugin_result* out, Ctrl* ctrl,
+                            int slot, int64_t tb, int64_t te, cudaStream_t s) {
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_kernel<R, ORDER>, kPsiThreads, 0);
+    grid_cap = sms * (occ > 0 ? occ : 1);
+  }
+  int64_t tiles = te - tb;
+  int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
+  if (grid < 1) grid = 1;
+  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, mode, g, out, ctrl, slot, tb, te);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_psi(const float* xs, int64_t n, int r, int mode, double g_host, const plugin_result* out,
+                       Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, cudaStream_t s) {
+  const int R = psi_rows_per_thread(n);
+  if (tile_end <= tile_begin) return cudaSuccess;
+#define PLG_CASE(RR)                                                                              \
+  if (R == RR) {                                                                                  \
+    return r == 6 ? launch_t<RR, 6>(xs, n, mode, g_host, out, ctrl, slot, tile_begin, tile_end, s) \
+                  : launch_t<RR, 4>(xs, n, mode, g_host, out, ctrl, slot, tile_begin, tile_end, s); \
+  }
+  PLG_CASE(8)
+  PLG_CASE(4)
+  PLG_CASE(2)
+  PLG_CASE(1)
+#undef PLG_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace plg

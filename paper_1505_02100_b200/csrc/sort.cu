@@ -1,0 +1,165 @@
+// sort.cu -- ascending sort of the float32 sample into the workspace.
+//
+// Not a step of Algorithm 1: Psi_r is a symmetric sum, so the order of X is free.
+// Sorting fixes the summation order so that (a) every fp32 chunk the psi pass adds
+// holds terms of similar size (no absorption of the small far-tail terms by a large
+// running sum) and (b) tiles of the pair triangle map to bands of |u|.
+// Sorting values (not key/value pairs) gives a unique output array, so the result
+// is deterministic.  LSD radix sort, 4 passes of 8 bits; each pass: per-tile digit
+// histograms, one exclusive scan, and a stable scatter (the tile is ordered by the
+// digit with 8 stable 1-bit splits in shared memory).
+#include "common.cuh"
+
+namespace plg {
+
+// Order-preserving float -> uint32 key, on the raw bits (loaded as integers: written on
+// floats, nvcc turns `bits | 0x80000000` into an FADD -|x| that canonicalises NaN payloads).
+__device__ __forceinline__ unsigned int bits2key(unsigned int b) {
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ unsigned int key2bits(unsigned int k) {
+  return (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ unsigned int load_key(const void* src, int64_t i) {
+  const unsigned int v = __ldg(reinterpret_cast<const unsigned int*>(src) + i);
+  return FIRST ? bits2key(v) : v;
+}
+
+// per-tile histogram of digit (key >> shift) & 255, stored digit-major: hist[d * nb + b]
+template <bool FIRST>
+__global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const void* src, int64_t n, int shift,
+                                                                 unsigned int* hist, int64_t nb) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  for (int q = threadIdx.x; q < kSortTile; q += kSortThreads) {
+    int64_t i = base + q;
+    if (i < n) atomicAdd(&h[(load_key<FIRST>(src, i) >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
+}
+
+// block-wide exclusive scan of one value per thread (1024 threads max)
+template <int NT>
+__device__ __forceinline__ unsigned int block_excl_scan(unsigned int v, unsigned int* warp_tot, unsigned int& total) {
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned int inc = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (l >= o) inc += y;
+  }
+  if (l == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned int t = (l < NT / 32) ? warp_tot[l] : 0u;
+    unsigned int ti = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned int y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (l >= o) ti += y;
+    }
+    if (l < NT / 32) warp_tot[l] = ti - t;  // exclusive warp offsets
+    if (l == 31) warp_tot[32] = ti;
+  }
+  __syncthreads();
+  unsigned int r = warp_tot[w] + inc - v;
+  total = warp_tot[32];
+  __syncthreads();
+  return r;
+}
+
+// exclusive scan of hist (length m) in place, single CTA of 1024 threads, coalesced rounds
+__global__ void __launch_bounds__(1024) sort_scan_kernel(unsigned int* hist, int64_t m) {
+  __shared__ unsigned int wt[33];
+  unsigned int carry = 0;
+  for (int64_t base = 0; base < m; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const unsigned int v = (i < m) ? hist[i] : 0u;
+    unsigned int tot;
+    const unsigned int off = block_excl_scan<1024>(v, wt, tot);
+    if (i < m) hist[i] = carry + off;
+    carry += tot;
+  }
+}
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const void* src, int64_t n, int shift,
+                                                                    const unsigned int* __restrict__ offs,
+                                                                    int64_t nb, void* dst) {
+  constexpr int IPT = kSortTile / kSortThreads;  // 16 keys per thread, blocked arrangement
+  __shared__ unsigned int bufA[kSortTile];
+  __shared__ unsigned int bufB[kSortTile];
+  __shared__ unsigned int wt[33];
+  __shared__ unsigned int dstart[256];
+  __shared__ unsigned int dcount[256];
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const int cnt = (int)((n - base) < kSortTile ? (n - base) : kSortTile);
+  for (int q = threadIdx.x; q < kSortTile; q += kSortThreads)
+    bufA[q] = (q < cnt) ? load_key<FIRST>(src, base + q) : 0xffffffffu;  // pads sort last
+  dcount[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned int* in = bufA;
+  unsigned int* out = bufB;
+  for (int bit = 0; bit < 8; ++bit) {
+    unsigned int k[IPT];
+    unsigned int zeros = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      k[q] = in[threadIdx.x * IPT + q];
+      zeros += ((k[q] >> (shift + bit)) & 1u) ^ 1u;
+    }
+    unsigned int Z;
+    unsigned int zpre = block_excl_scan<kSortThreads>(zeros, wt, Z);
+    unsigned int opre = threadIdx.x * IPT - zpre;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      unsigned int one = (k[q] >> (shift + bit)) & 1u;
+      unsigned int pos = one ? Z + opre : zpre;
+      out[pos] = k[q];
+      opre += one;
+      zpre += one ^ 1u;
+    }
+    __syncthreads();
+    unsigned int* t = in;
+    in = out;
+    out = t;
+  }
+  // tile is now ordered by digit (stable); local start of each digit
+  for (int q = threadIdx.x; q < cnt; q += kSortThreads) atomicAdd(&dcount[(in[q] >> shift) & 255u], 1u);
+  __syncthreads();
+  unsigned int tot;
+  unsigned int st = block_excl_scan<kSortThreads>(dcount[threadIdx.x], wt, tot);
+  dstart[threadIdx.x] = st;
+  __syncthreads();
+  for (int q = threadIdx.x; q < cnt; q += kSortThreads) {
+    unsigned int key = in[q];
+    unsigned int d = (key >> shift) & 255u;
+    int64_t o = (int64_t)offs[(int64_t)d * nb + blockIdx.x] + (q - (int)dstart[d]);
+    reinterpret_cast<unsigned int*>(dst)[o] = LAST ? key2bits(key) : key;
+  }
+}
+
+// x (float) -> xs (float, ascending).  tmp: n uint32; hist: 256*nb uint32.
+// Passes ping-pong tmp <-> xs (reinterpreted as keys); the last pass writes floats into xs.
+cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
+                        int64_t nb, cudaStream_t s) {
+  unsigned int* xk = reinterpret_cast<unsigned int*>(xs);
+  const void* src = x;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    void* dst = (pass & 1) ? (void*)xk : (void*)tmp;   // 0: x->tmp, 1: tmp->xs, 2: xs->tmp, 3: tmp->xs
+    if (pass == 0) sort_hist_kernel<true><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
+    else sort_hist_kernel<false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
+    sort_scan_kernel<<<1, 1024, 0, s>>>(hist, 256 * nb);
+    if (pass == 0) sort_scatter_kernel<true, false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    else if (pass == 3) sort_scatter_kernel<false, true><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    else sort_scatter_kernel<false, false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    src = dst;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace plg

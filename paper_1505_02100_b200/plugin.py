@@ -1,0 +1,214 @@
+"""Thin ctypes binding of libplugin.so (include/plugin.h).  Argument marshalling only:
+every step of the method runs in the library's CUDA kernels.  There is no CPU
+fallback: if the library or a CUDA device is missing, calls raise.
+
+Tensors are torch tensors (torch is used for device memory and streams only).
+Function names match the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libplugin.so")
+
+PLUGIN_OK, PLUGIN_E_INVALID, PLUGIN_E_NONFINITE, PLUGIN_E_DEGENERATE, PLUGIN_E_DOMAIN, PLUGIN_E_CUDA = range(6)
+STATUS_NAMES = {0: "PLUGIN_OK", 1: "PLUGIN_E_INVALID", 2: "PLUGIN_E_NONFINITE", 3: "PLUGIN_E_DEGENERATE",
+                4: "PLUGIN_E_DOMAIN", 5: "PLUGIN_E_CUDA"}
+
+
+class PluginError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class plugin_result(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n", ctypes.c_int64)] + [
+        (k, ctypes.c_double) for k in ("mean", "var", "sigma", "psi8_ns", "g1", "psi6", "g2", "psi4", "h",
+                                       "g1_z", "psi6_z", "g2_z", "psi4_z", "h_z", "S6", "S4")]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+class plugin_fx128(ctypes.Structure):
+    _fields_ = [("limb", ctypes.c_int64 * 4)]
+
+
+RESULT_BYTES = ctypes.sizeof(plugin_result)
+_lib = None
+
+
+def lib():
+    """Load libplugin.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, i32, sz, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_double
+        sig = {
+            "plugin_workspace_bytes": (sz, [i64]),
+            "plugin_host_workspace_bytes": (sz, [i64]),
+            "plugin_h": (i32, [P, i64, P, P, sz, P]),
+            "plugin_h_sync": (i32, [P, i64, P, P, sz, P]),
+            "plugin_h_host": (i32, [P, i64, P, P, sz, P]),
+            "psi_r": (i32, [P, i64, d, i32, P, P, sz, P]),
+            "plugin_step1": (i32, [P, i64, P, P, sz, P]),
+            "psi_r_shard": (i32, [i64, i32, i32, i32, P, P, P, sz, P]),
+            "plugin_after_psi6": (i32, [P, P, P]),
+            "plugin_after_psi4": (i32, [P, P, P]),
+            "plugin_num_tiles": (i64, [i64]),
+            "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "plugin_last_error": (ctypes.c_char_p, []),
+            "plugin_version": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_sync", "plugin_h_host",
+            "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
+            "plugin_shard_tiles", "plugin_last_error", "plugin_version")
+
+
+def _check(st: int):
+    if st == PLUGIN_E_INVALID or st == PLUGIN_E_CUDA:
+        raise PluginError(st, lib().plugin_last_error().decode())
+    return st
+
+
+def _stream(stream):
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _x(x: torch.Tensor) -> torch.Tensor:
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 and x.dim() == 1):
+        raise TypeError("x must be a 1-D CUDA float32 tensor")
+    return x.contiguous()
+
+
+def plugin_workspace_bytes(n: int) -> int:
+    return lib().plugin_workspace_bytes(n)
+
+
+def plugin_host_workspace_bytes(n: int) -> int:
+    return lib().plugin_host_workspace_bytes(n)
+
+
+def workspace(n: int, device=None, host: bool = False) -> torch.Tensor:
+    """A 256-byte aligned uint8 device buffer of the size the library needs."""
+    nbytes = plugin_host_workspace_bytes(n) if host else plugin_workspace_bytes(n)
+    t = torch.empty(nbytes + 256, dtype=torch.uint8, device=device or "cuda")
+    off = (-t.data_ptr()) % 256
+    return t[off:off + nbytes]
+
+
+def new_result(device=None) -> torch.Tensor:
+    return torch.empty(RESULT_BYTES, dtype=torch.uint8, device=device or "cuda")
+
+
+def read_result(buf: torch.Tensor) -> dict:
+    """Copy a device plugin_result to the host (synchronises) and decode it."""
+    h = buf.detach().to("cpu").numpy().tobytes()
+    return plugin_result.from_buffer_copy(h).to_dict()
+
+
+def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """Alg. 1 on the device (asynchronous).  Returns the device result buffer."""
+    x = _x(x)
+    n = x.numel()
+    ws = workspace(n, x.device) if ws is None else ws
+    out = new_result(x.device) if out is None else out
+    _check(lib().plugin_h(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
+def plugin_h_sync(x: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> dict:
+    x = _x(x)
+    n = x.numel()
+    ws = workspace(n, x.device) if ws is None else ws
+    res = plugin_result()
+    _check(lib().plugin_h_sync(x.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return res.to_dict()
+
+
+def plugin_h_host(x_host: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """End to end from host memory (copies inside the call)."""
+    if not (isinstance(x_host, torch.Tensor) and not x_host.is_cuda and x_host.dtype == torch.float32):
+        raise TypeError("x_host must be a CPU float32 tensor (pinned for best speed)")
+    x_host = x_host.contiguous()
+    n = x_host.numel()
+    ws = workspace(n, "cuda", host=True) if ws is None else ws
+    res = plugin_result()
+    _check(lib().plugin_h_host(x_host.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(),
+                               _stream(stream)))
+    return res.to_dict()
+
+
+def psi_r(x: torch.Tensor, g: float, r: int, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+          stream=None) -> torch.Tensor:
+    """Psi_r(g) (Steps IV/VI) as a device float64[1] tensor (asynchronous)."""
+    x = _x(x)
+    n = x.numel()
+    ws = workspace(n, x.device) if ws is None else ws
+    out = torch.empty(1, dtype=torch.float64, device=x.device) if out is None else out
+    _check(lib().psi_r(x.data_ptr(), n, float(g), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
+def plugin_step1(x: torch.Tensor, out: torch.Tensor, ws: torch.Tensor, stream=None):
+    x = _x(x)
+    _check(lib().plugin_step1(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
+def new_partial(device=None) -> torch.Tensor:
+    return torch.empty(4, dtype=torch.int64, device=device or "cuda")
+
+
+def psi_r_shard(n: int, r: int, rank: int, world: int, out: torch.Tensor, partial: torch.Tensor, ws: torch.Tensor,
+                stream=None):
+    _check(lib().psi_r_shard(n, r, rank, world, out.data_ptr(), partial.data_ptr(), ws.data_ptr(), ws.numel(),
+                             _stream(stream)))
+    return partial
+
+
+def plugin_after_psi6(total: torch.Tensor, out: torch.Tensor, stream=None):
+    _check(lib().plugin_after_psi6(total.data_ptr(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def plugin_after_psi4(total: torch.Tensor, out: torch.Tensor, stream=None):
+    _check(lib().plugin_after_psi4(total.data_ptr(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def plugin_num_tiles(n: int) -> int:
+    return lib().plugin_num_tiles(n)
+
+
+def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    lib().plugin_shard_tiles(n, rank, world, ctypes.byref(b), ctypes.byref(e))
+    return b.value, e.value
+
+
+def plugin_last_error() -> str:
+    return lib().plugin_last_error().decode()
+
+
+def plugin_version() -> str:
+    return lib().plugin_version().decode()

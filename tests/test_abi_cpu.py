@@ -1,0 +1,67 @@
+"""CPU-only checks of the C ABI boundary: libplugin.so loads, exports every symbol the
+header declares, and its pure host-side functions (workspace sizing, tile sharding)
+behave.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "plugin.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1505_02100_b200 import plugin
+    return plugin
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(plugin_\w+|psi_r\w*)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("plugin_h", "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4",
+                 "plugin_workspace_bytes", "plugin_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(_declared()) == set(L.EXPORTED)
+
+
+def test_version_and_error_strings(L):
+    assert "sm_100a" in L.plugin_version()
+    assert L.plugin_last_error() == ""
+
+
+def test_workspace_sizes_monotone(L):
+    prev = 0
+    for n in (1, 2, 1000, 4096, 4097, 1 << 20, 1 << 22):
+        b = L.plugin_workspace_bytes(n)
+        assert b >= 8 * n and b >= prev and b % 256 == 0
+        assert L.plugin_host_workspace_bytes(n) >= b + 4 * n
+        prev = b
+
+
+@pytest.mark.parametrize("n", [1, 2, 255, 256, 257, 16384, 131072, 1 << 20, 4194304])
+def test_tiles_cover_triangle(L, n):
+    w = L.plugin_num_tiles(n)
+    assert w >= 1
+    for world in (1, 2, 3, 4, 8):
+        spans = [L.plugin_shard_tiles(n, r, world) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == w
+        for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
+            assert e0 == b1
+        sizes = [e - b for b, e in spans]
+        assert max(sizes) - min(sizes) <= 1           # equal-work tiles, balanced to one tile
+    assert L.plugin_shard_tiles(n, 3, 2) == (0, 0)    # invalid rank -> empty range

@@ -15,3 +15,6 @@ def cfg(k):
         c = r.integers(0, 5, n); z = r.standard_normal(n); return mu[c] + sd[c] * z
 for k in range(1, 6):
     cfg(k).astype(np.float32).tofile(f"{out}/cfg{k}.f32")
+# adversarial extras (same recipes as paper_1505_02100_b200/inputs.py)
+r = np.random.default_rng(4); (np.round(r.standard_normal(12000) * 37 / 6.0) * (6.0 / 37)).astype(np.float32).tofile(f"{out}/ties.f32")
+r = np.random.default_rng(5); (1.0e6 + r.standard_normal(12000)).astype(np.float32).tofile(f"{out}/offset.f32")
