@@ -23,11 +23,22 @@
 // fp32 accumulators hold 16 terms per lane, then go to per-row fp64; each tile's fp64
 // total is added as a 128-bit fixed-point integer, so the result does not depend on
 // tile scheduling, grid size or GPU count.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace plg {
 
 typedef unsigned long long u64;
+
+// fp32 chunk length (j per flush to fp64) and unroll of the j loop; -D overrides are tuning only
+#ifndef PSI_CH
+#define PSI_CH 64
+#endif
+#ifndef PSI_UNROLL
+#define PSI_UNROLL 16
+#endif
+constexpr int kPsiUnroll = PSI_UNROLL;
 
 __device__ __forceinline__ u64 pk2(float a, float b) {
   u64 r;
@@ -145,12 +156,16 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
   bj = b + (t - (b * nb - b * (b - 1) / 2));
 }
 
+// min resident CTAs per SM for the register budget: R=8 -> 2 (<=128 regs), R<=4 -> 3 (<=80 regs)
+template <int R>
+struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : 3; };
+
 template <int R, int ORDER>
-__global__ void __launch_bounds__(kPsiThreads, 2)
+__global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, const plugin_result* __restrict__ out,
            Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
   constexpr int T = kPsiThreads * R;
-  constexpr int CH = 64;  // j per fp32 chunk (32 per packed lane) before the fp64 flush
+  constexpr int CH = PSI_CH;  // j per fp32 chunk (CH/2 per packed lane) before the fp64 flush
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
@@ -205,7 +220,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, con
       u64 acc[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) acc[k] = 0ull;
-#pragma unroll 2
+#pragma unroll kPsiUnroll
       for (int q = 0; q < CH / 4; ++q) {
         const float4 v = sx4[c * (CH / 4) + q];
         const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
@@ -275,6 +290,10 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, con
 }
 
 int psi_rows_per_thread(int64_t n) {
+  if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2 or 1)
+    int r = atoi(e);
+    if (r == 8 || r == 4 || r == 2 || r == 1) return r;
+  }
   // largest R in {8,4,2} whose tile count keeps >= ~28 tiles per resident CTA (296 on 148 SMs)
   const int cand[3] = {8, 4, 2};
   for (int c : cand) {

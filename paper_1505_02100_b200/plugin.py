@@ -13,7 +13,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libplugin.so")
+LIB_PATH = os.environ.get("PLUGIN_LIB_PATH") or os.path.join(HERE, "libplugin.so")
 
 PLUGIN_OK, PLUGIN_E_INVALID, PLUGIN_E_NONFINITE, PLUGIN_E_DEGENERATE, PLUGIN_E_DOMAIN, PLUGIN_E_CUDA = range(6)
 STATUS_NAMES = {0: "PLUGIN_OK", 1: "PLUGIN_E_INVALID", 2: "PLUGIN_E_NONFINITE", 3: "PLUGIN_E_DEGENERATE",
