@@ -76,6 +76,8 @@ def lib():
         L.oracle_widen.argtypes = [P, i64, P]
         L.oracle_psi_rows.restype = None
         L.oracle_psi_rows.argtypes = [P, i64, d, i32, i64, i64, i32, P]
+        L.oracle_psi_block.restype = None
+        L.oracle_psi_block.argtypes = [P, i64, d, i32, i64, i64, i64, i64, i32, P]
         L.oracle_psi_literal_sum.restype = d
         L.oracle_psi_literal_sum.argtypes = [P, i64, d, i32]
         L.oracle_max_threads.restype = i32
@@ -245,6 +247,15 @@ def psi(z, g: float, r: int, threads: int = 0, checkpoint: str | None = None, lo
     z = np.ascontiguousarray(z, dtype=np.float64)
     T = psi_halved_sum(z, g, r, threads, checkpoint, log)
     return psi_from_halved_sum(T, z.size, g, r)
+
+
+def psi_block_sum(z, g: float, r: int, i0: int, i1: int, j0: int, j1: int, threads: int = 0) -> float:
+    """sum_{i0<=i<i1} sum_{j0<=j<j1} K^(r)((z_i - z_j)/g): a block of the double sum of Steps IV/VI."""
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.zeros(2, dtype=np.float64)
+    lib().oracle_psi_block(_ptr(z), z.size, float(g), int(r), int(i0), int(i1), int(j0), int(j1), int(threads),
+                           _ptr(out))
+    return float(out[0]) + float(out[1])
 
 
 def psi_literal(z, g: float, r: int) -> float:

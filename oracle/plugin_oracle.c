@@ -140,6 +140,38 @@ void oracle_psi_rows(const double* z, int64_t n, double g, int r, int64_t i0, in
 }
 
 /*
+ * A rectangular block of the literal double sum of Steps IV/VI:
+ * sum_{i0<=i<i1} sum_{j0<=j<j1} K^(r)((z_i - z_j)/g), per-row Neumaier, rows combined
+ * in index order (OpenMP over rows; bit-identical for any thread count).
+ * Used to check sampled blocks of a full-size pass one by one.
+ */
+void oracle_psi_block(const double* z, int64_t n, double g, int r, int64_t i0, int64_t i1,
+                      int64_t j0, int64_t j1, int nthreads, double* out) {
+  if (i0 < 0) i0 = 0;
+  if (j0 < 0) j0 = 0;
+  if (i1 > n) i1 = n;
+  if (j1 > n) j1 = n;
+  out[0] = 0.0; out[1] = 0.0;
+  if (i1 <= i0 || j1 <= j0) return;
+  int64_t m = i1 - i0;
+  double* row = (double*)malloc(sizeof(double) * (size_t)m);
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t k = 0; k < m; ++k) {
+    int64_t i = i0 + k;
+    neumaier_t acc = {0, 0};
+    for (int64_t j = j0; j < j1; ++j) neumaier_add(&acc, oracle_K(r, (z[i] - z[j]) / g));
+    row[k] = neumaier_value(&acc);
+  }
+  neumaier_t tot = {0, 0};
+  for (int64_t k = 0; k < m; ++k) neumaier_add(&tot, row[k]);
+  free(row);
+  out[0] = tot.s; out[1] = tot.c;
+}
+
+/*
  * The literal full double sum of Alg. 1 Step IV/VI:
  * sum_{i=1..n} sum_{j=1..n} K^(r)((z_i - z_j)/g), Neumaier in (i, j) order.
  * Used for small n to check the halving of Eq. 5-7.

@@ -178,3 +178,66 @@ def test_argument_errors(P):
             P.psi_r(x, bad["g"], bad["r"])
     with pytest.raises(P.PluginError, match="workspace too small"):
         P.plugin_h(x, ws=P.workspace(10))
+
+
+def _tile_coords(t, nb):
+    # row-major upper block triangle incl. the diagonal (the order psi_r_shard walks)
+    b = 0
+    lo, hi = 0, nb - 1
+    while lo < hi:                       # largest b with off(b) <= t, off(b) = b*nb - b(b-1)/2
+        mid = (lo + hi + 1) // 2
+        if mid * nb - mid * (mid - 1) // 2 <= t:
+            lo = mid
+        else:
+            hi = mid - 1
+    b = lo
+    return b, b + (t - (b * nb - b * (b - 1) // 2))
+
+
+@pytest.mark.parametrize("k", [4, 5])
+def test_full_size_sampled_tile_shards(P, oracle_mod, k):
+    """Full-size configs in the launch configuration bench.py times: sampled tile ranges of
+    both passes (psi_r_shard, exact fixed-point partials) against the oracle's block sums of
+    the same pairs.  Bandwidths come from the oracle: g1 (Steps I-III, closed form) for r=6
+    and 0.2 sigma for r=4 (the identity checked holds at any g)."""
+    from paper_1505_02100_b200.distributed import from_limbs
+    x = inputs.config_data(k)
+    n = x.size
+    s1 = oracle_mod.step1(x)
+    sigma = s1["sigma"]
+    g1 = oracle_mod.g1_bandwidth(oracle_mod.psi8_ns(1.0), n) * sigma
+    g4 = 0.2 * sigma
+    xd = torch.from_numpy(x).cuda()
+    ws = P.workspace(n)
+    P.plugin_step1(xd, P.new_result(), ws)           # sorts X into the workspace
+    res = P.plugin_result()
+    res.status, res.n, res.g1, res.g2 = 0, n, g1, g4
+    dres = torch.frombuffer(bytearray(bytes(res)), dtype=torch.uint8).cuda()
+    zs = np.sort(oracle_mod.widen(x))
+    ntiles = P.plugin_num_tiles(n)
+    nb = int(round((-1 + math.sqrt(1 + 8 * ntiles)) / 2))
+    assert nb * (nb + 1) // 2 == ntiles
+    T = -(-n // nb)
+    T = next(t for t in (256, 512, 1024, 2048) if -(-n // t) == nb and t >= T)
+    world = 1024
+    phi0 = 1 / math.sqrt(2 * math.pi)
+    for r, g in ((6, g1), (4, g4)):
+        for rank in (0, world // 2, world - 1):
+            part = P.new_partial()
+            P.psi_r_shard(n, r, rank, world, dres, part, ws)
+            got = from_limbs(part.cpu().tolist()) / 2.0 ** 64 * phi0
+            tb, te = P.plugin_shard_tiles(n, rank, world)
+            runs = {}                       # tile row bi -> (first bj, last bj) of this shard
+            for t in range(tb, te):
+                bi, bj = _tile_coords(t, nb)
+                lo, hi = runs.get(bi, (bj, bj))
+                runs[bi] = (min(lo, bj), max(hi, bj))
+            ref = 0.0
+            for bi, (lo, hi) in runs.items():
+                rows = (bi * T, min(n, bi * T + T))
+                if lo == bi:                # diagonal tile: full square, weight 1
+                    ref += oracle_mod.psi_block_sum(zs, g, r, *rows, bi * T, min(n, bi * T + T))
+                    lo += 1
+                if lo <= hi:                # off-diagonal tiles: weight 2
+                    ref += 2.0 * oracle_mod.psi_block_sum(zs, g, r, *rows, lo * T, min(n, hi * T + T))
+            assert rel(got, ref) < TOL, (k, r, rank, got, ref, rel(got, ref))

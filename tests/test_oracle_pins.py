@@ -361,3 +361,18 @@ def test_normal_sample_expectation(oracle_mod, r, g):
 def test_config_inputs_sha256():
     for k in (1, 2, 3):
         assert inputs.sha256_f32(inputs.config_data(k)) == inputs.SHA256[k]
+
+
+def test_block_sums_partition_the_double_sum(oracle_mod):
+    # the rectangular blocks used for sampled full-size parity add up to the literal double sum,
+    # and full = 2 * (upper blocks) + (diagonal blocks)  (Eq. 5-7)
+    z = np.random.default_rng(12).standard_normal(301)
+    n, g = z.size, 0.45
+    cuts = [0, 77, 150, 301]
+    for r in (4, 6):
+        lit = oracle_mod.lib().oracle_psi_literal_sum(z.ctypes.data, n, g, r)
+        blocks = {(a, b): oracle_mod.psi_block_sum(z, g, r, cuts[a], cuts[a + 1], cuts[b], cuts[b + 1])
+                  for a in range(3) for b in range(3)}
+        assert sum(blocks.values()) == pytest.approx(lit, rel=1e-13)
+        sym = sum(2 * v if a < b else v for (a, b), v in blocks.items() if a <= b)
+        assert sym == pytest.approx(lit, rel=1e-13)
