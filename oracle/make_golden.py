@@ -2,7 +2,7 @@
 
 Calls only oracle/ (and the seeded input generators).  Long configs checkpoint per
 row chunk under tests/golden/checkpoints/ so a run can resume.
-usage: python -m oracle.make_golden 1 2 3 [--threads T]
+usage: python -m oracle.make_golden 1 2 3 [--threads T] [--ckpt-root DIR] [--out-dir DIR]
 """
 import argparse
 import hashlib
@@ -42,12 +42,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+", type=int)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--ckpt-root", default=os.path.join(ROOT, "tests", "golden", "checkpoints"))
+    ap.add_argument("--out-dir", default=os.path.join(ROOT, "tests", "golden"))
     a = ap.parse_args()
     for k in a.configs:
         x = inputs.config_data(k)
         sha = inputs.sha256_f32(x)
         assert sha == inputs.SHA256[k], f"cfg{k} input hash mismatch"
-        ck = os.path.join(ROOT, "tests", "golden", "checkpoints", f"cfg{k}")
+        ck = os.path.join(a.ckpt_root, f"cfg{k}")
         os.makedirs(ck, exist_ok=True)
         t0 = time.time()
         res = oracle.plugin(x, threads=a.threads, checkpoint_dir=ck, log=lambda m: print(m, flush=True))
@@ -55,7 +57,8 @@ def main():
         res.update({"config": k, "sha256": sha, "oracle_src": _src_hash(), "cpu": cpu_model(),
                     "wall_seconds": time.time() - t0,
                     "written_by": "python -m oracle.make_golden (oracle/ only)"})
-        out = os.path.join(ROOT, "tests", "golden", f"cfg{k}.json")
+        os.makedirs(a.out_dir, exist_ok=True)
+        out = os.path.join(a.out_dir, f"cfg{k}.json")
         with open(out, "w") as f:
             json.dump(res, f, indent=1, sort_keys=True)
         print(f"cfg{k}: h={res['h']!r} psi6_z={res['psi6_z']!r} psi4_z={res['psi4_z']!r} ({res['wall_seconds']:.1f}s)", flush=True)
