@@ -101,6 +101,18 @@ class ClockSampler:
                 "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
 
 
+def _traffic(n):
+    """DRAM bytes per psi launch from the committed ncu --set full capture (same n only)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "psi_traffic.json")) as f:
+            t = json.load(f)
+    except OSError:
+        return None
+    if t.get("n") != n:
+        return None
+    return t["dram_bytes_read_per_launch"] + t["dram_bytes_write_per_launch"]
+
+
 def cpu_oracle_sample(k: int, seconds: float, threads: int = 0):
     """Time the oracle (as it stands) on rows [0, m) of both passes of config k."""
     import numpy as np
@@ -257,7 +269,7 @@ def run_ours(a):
                        "parallelism": f"tile-triangle shards x{world}, 1 NCCL allreduce (32 B) per pass"
                        if world > 1 else "single GPU"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
-                         "traffic": None, "kernel": "psi_kernel (r=6 and r=4 pass average)",
+                         "traffic": _traffic(n), "kernel": "psi_kernel (r=6 and r=4 pass average)",
                          "peak_basis": f"{MUFU_EX2_PER_CLK_PER_SM} MUFU.EX2/clk/SM x {sms} SMs x measured median "
                                        f"SM clock {f_meas:.0f} MHz (1 ex2 per pair)",
                          "frac_at_1965MHz": achieved / (MUFU_EX2_PER_CLK_PER_SM * sms * 1.965)},

@@ -80,6 +80,8 @@ def lib():
         L.oracle_psi_block.argtypes = [P, i64, d, i32, i64, i64, i64, i64, i32, P]
         L.oracle_psi_literal_sum.restype = d
         L.oracle_psi_literal_sum.argtypes = [P, i64, d, i32]
+        L.oracle_kde.restype = None
+        L.oracle_kde.argtypes = [P, i64, d, P, i64, i32, P]
         L.oracle_max_threads.restype = i32
         L.oracle_max_threads.argtypes = []
         _lib = L
@@ -263,6 +265,21 @@ def psi_literal(z, g: float, r: int) -> float:
     z = np.ascontiguousarray(z, dtype=np.float64)
     n = z.size
     return lib().oracle_psi_literal_sum(_ptr(z), n, float(g), int(r)) / (n * n * g ** (r + 1))
+
+
+# ---- Eq. 1-2: the kernel density estimate that h is for ----------
+def kde(x, h: float, points, threads: int = 0) -> np.ndarray:
+    """Eq. 1 with Eq. 2: f(x_k, h) = (1/(n h)) sum_i K((x_k - X_i)/h), fp64.
+
+    ``x`` is the float32 sample, ``points`` the evaluation points (float32 values
+    are widened exactly, as the GPU reads them)."""
+    x = _f32(x)
+    if not (h > 0.0 and math.isfinite(h)):
+        raise OracleError("E_INVALID", f"h = {h!r} must be finite and > 0")
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    f = np.empty(pts.size, dtype=np.float64)
+    lib().oracle_kde(_ptr(x), x.size, float(h), _ptr(pts), pts.size, int(threads), _ptr(f))
+    return f
 
 
 # ---- the whole Algorithm 1 -------------------------------------------------------------

@@ -183,6 +183,26 @@ double oracle_psi_literal_sum(const double* z, int64_t n, double g, int r) {
   return neumaier_value(&acc);
 }
 
+/*
+ * Eq. 1 with the Gaussian kernel of Eq. 2: the kernel density
+ * estimator f(x, h) = (1/(n h)) sum_{i=1..n} K((x - X_i)/h) at m points x_k.
+ * Literal: for every point a Neumaier sum over i in index order of
+ * exp(-u^2/2)/sqrt(2 pi) with u = (x_k - X_i)/h, then one division by n h.
+ * OpenMP over points (independent; bit-identical for any thread count).
+ */
+void oracle_kde(const float* X, int64_t n, double h, const double* xk, int64_t m, int nthreads,
+                double* f) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 4)
+#endif
+  for (int64_t k = 0; k < m; ++k) {
+    neumaier_t acc = {0, 0};
+    for (int64_t i = 0; i < n; ++i) neumaier_add(&acc, oracle_phi((xk[k] - (double)X[i]) / h));
+    f[k] = neumaier_value(&acc) / ((double)n * h);
+  }
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
