@@ -43,6 +43,12 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--workload", default="plugin", choices=["plugin", "kde"],
+                    help="plugin: Alg. 1 (the headline); kde: Eq. 1-2 on a 65536-point curve (NEXT 1)")
+    ap.add_argument("--kde-points", type=int, default=65536)
+    ap.add_argument("--skip-underflow", action="store_true",
+                    help="plugin workload, 1 GPU: PLUGIN_SKIP_UNDERFLOW (bit-identical result; reports the "
+                         "effective rate, the roofline over the pairs actually evaluated)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     return ap.parse_args()
@@ -172,6 +178,78 @@ def run_reference(a):
     return 0
 
 
+def psi_pairs_evaluated(xh, g, tile=2048):
+    """Pairs the psi pass evaluates with PLUGIN_SKIP_UNDERFLOW (the rule of psi.cu): every
+    diagonal tile, and off-diagonal tiles unless (xs[j0] - xs[i0+T-1]) s (1 - 1e-5) > 13.25."""
+    import numpy as np
+    xs = np.sort(xh.astype(np.float32)).astype(np.float64)
+    n = xs.size
+    nb = -(-n // tile)
+    s = float(np.float32(1.0 / g))
+    first = xs[np.arange(nb) * tile]
+    last = xs[np.minimum(np.arange(nb) * tile + tile - 1, n - 1)]
+    rows = np.minimum(tile, n - np.arange(nb) * tile).astype(np.float64)
+    tot = 0.0
+    for bi in range(nb):
+        gap = first[bi + 1:] - last[bi]
+        keep = ~(gap * s * (1 - 1e-5) > 13.25)
+        tot += 2.0 * rows[bi] * float(np.sum(rows[bi + 1:][keep])) / 2.0  # unique pairs (i<j) of kept tiles
+        tot += rows[bi] * (rows[bi] - 1) / 2.0
+    return tot
+
+
+def run_skip(a):
+    """1 GPU, plugin_h_ex(PLUGIN_SKIP_UNDERFLOW): effective pair rate, bit-identical result."""
+    import torch
+
+    from paper_1505_02100_b200 import inputs
+    from paper_1505_02100_b200 import plugin as P
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    xh = inputs.config_data(a.config)
+    n = xh.size
+    x = torch.from_numpy(xh).to(dev)
+    ws = P.workspace(n, dev)
+    out = P.new_result(dev)
+    ref = P.read_result(P.plugin_h(x, out=out, ws=ws))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(a.warmup):
+        P.plugin_h(x, out=out, ws=ws, flags=P.PLUGIN_SKIP_UNDERFLOW)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    for s in range(a.steps):
+        flush.fill_(s & 0xff)
+        ev[s][0].record(stream)
+        P.plugin_h(x, out=out, ws=ws, flags=P.PLUGIN_SKIP_UNDERFLOW)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    res = P.read_result(out)
+    same = all(res[k] == ref[k] for k in ref if ref[k] == ref[k])
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.steps
+    pairs = n * (n - 1) // 2
+    ev6, ev4 = psi_pairs_evaluated(xh, res["g1"]), psi_pairs_evaluated(xh, res["g2"])
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_meas = clocks.get("sm_mhz") or 1965.0
+    peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
+    line = {"metric": METRIC + " [effective, PLUGIN_SKIP_UNDERFLOW]", "value": 2 * pairs / (ms / 1e3) / 1e9,
+            "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": _workload(a.config, n) + " with PLUGIN_SKIP_UNDERFLOW", "n": n,
+                       "pairs_per_step_effective": 2 * pairs, "pairs_evaluated": {"psi6": ev6, "psi4": ev4},
+                       "bit_identical_to_full": same},
+            "roofline": {"bound": "alu", "achieved": (ev6 + ev4) / (ms / 1e3) / 1e9, "peak": peak, "unit": UNIT,
+                         "frac": (ev6 + ev4) / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "kernel": "whole step over evaluated pairs (includes sort/Step I)"},
+            "h": res["h"], "status": res["status"], "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * a.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -290,10 +368,110 @@ def run_ours(a):
     return 0
 
 
+KDE_H = {4: 0.1326215, 5: 0.05}   # fixed bandwidths (cfg4: its PLUGIN h rounded), as tests/test_gpu_kde.py
+
+
+def _kde_setup(k, m):
+    import numpy as np
+
+    from paper_1505_02100_b200 import inputs
+    xh = inputs.config_data(k)
+    h = KDE_H.get(k, 0.1)
+    pts = np.linspace(float(xh.min()) - 4 * h, float(xh.max()) + 4 * h, m).astype(np.float32)
+    return xh, h, pts
+
+
+def kde_terms_visited(xh, h, pts, block=1024):
+    """Terms kde_eval evaluates: per block of 1024 points, the sorted samples within the
+    fp32 underflow cutoff of the block's [min, max] (the same rule as kde.cu)."""
+    import numpy as np
+    xs = np.sort(xh.astype(np.float64))
+    kf = float(np.float32(-1.4426950408889634 / (2 * h * h)))
+    cut = (126.5 / abs(kf)) ** 0.5 * (1 + 1e-6)
+    tot = 0
+    for b in range(0, pts.size, block):
+        p = pts[b:b + block].astype(np.float64)
+        lo = np.searchsorted(xs, p.min() - cut, "left")
+        hi = np.searchsorted(xs, p.max() + cut, "right")
+        tot += p.size * max(0, hi - lo)
+    return tot
+
+
+def run_kde(a):
+    """Eq. 1-2 (NEXT 1): f(x_k, h) at a sorted 65536-point curve over BASELINE config k."""
+    import torch
+
+    from paper_1505_02100_b200 import plugin as P
+    xh, h, pts = _kde_setup(a.config, a.kde_points)
+    n, m = xh.size, pts.size
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    x = torch.from_numpy(xh).to(dev)
+    p = torch.from_numpy(pts).to(dev)
+    ws = P.kde_workspace(n, m, dev)
+    f = torch.empty(m, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(a.warmup):
+        P.kde_eval(x, h, p, out=f, ws=ws)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    for s in range(a.steps):
+        flush.fill_(s & 0xff)
+        ev[s][0].record(stream)
+        P.kde_eval(x, h, p, out=f, ws=ws)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in ev])
+    visited = kde_terms_visited(xh, h, pts)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_meas = clocks.get("sm_mhz") or 1965.0
+    peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
+    achieved = visited / (ms / 1e3) / 1e9
+    # end to end from host memory: H2D of X and the points, D2H of the curve
+    xpin, ppin = torch.from_numpy(xh).pin_memory(), torch.from_numpy(pts).pin_memory()
+    fh = torch.empty(m, dtype=torch.float64).pin_memory()
+    ts = []
+    for _ in range(max(3, min(a.steps, 10))):
+        flush.fill_(1)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        x.copy_(xpin, non_blocking=True)
+        p.copy_(ppin, non_blocking=True)
+        P.kde_eval(x, h, p, out=f, ws=ws)
+        fh.copy_(f, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        ts.append(time.perf_counter() - t0)
+    line = {"metric": "KDE terms/sec (Eq. 1-2, effective n*m)", "value": n * m / (ms / 1e3) / 1e9,
+            "unit": "GTerms/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"kde: cfg{a.config} n={n}, h={h}, {m} sorted points over [min-4h, max+4h]",
+                       "terms_visited": visited, "terms_effective": n * m,
+                       "l2": "flushed between steps (256 MiB write, outside the events)"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GTerms/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "kde_kernel",
+                         "peak_basis": f"{MUFU_EX2_PER_CLK_PER_SM} MUFU.EX2/clk/SM x {sms} SMs x {f_meas:.0f} MHz "
+                                       "(1 ex2 per visited term)"},
+            "e2e": {"value": n * m / statistics.median(ts) / 1e9, "unit": "GTerms/s",
+                    "h2d_bytes_per_step": 4 * (n + m), "d2h_bytes_per_step": 8 * m,
+                    "seconds_per_step": statistics.median(ts)},
+            "clocks": clocks, "gpu_launches": 14 * a.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     a = _args()
     if a.impl == "reference":
         return run_reference(a)
+    if a.workload == "kde":
+        return run_kde(a)
+    if a.skip_underflow:
+        return run_skip(a)
     return run_ours(a)
 
 

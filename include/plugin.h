@@ -88,6 +88,15 @@ size_t plugin_workspace_bytes(int64_t n);
 plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
                        void* d_ws, size_t ws_bytes, void* stream);
 
+/* plugin_h with option flags (0 = plugin_h).  PLUGIN_SKIP_UNDERFLOW: in both passes, skip
+ * the tiles of the sorted pair triangle in which every |X_i - X_j|/g exceeds 13.25: there
+ * every fp32 term is exactly zero (the exponent is below -127 and MUFU.EX2 flushes), so the
+ * result is bit-identical to plugin_h; only the work changes (the
+ * headline pair rate is always measured without it).  Unknown bits -> PLUGIN_E_INVALID. */
+#define PLUGIN_SKIP_UNDERFLOW 1u
+plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, unsigned int flags,
+                          void* d_ws, size_t ws_bytes, void* stream);
+
 /* Same as plugin_h (device result kept in the workspace), then synchronises `stream`,
  * copies the result to *h_out and returns its data status (PLUGIN_OK or one of
  * E_NONFINITE/E_DEGENERATE/E_DOMAIN). */
@@ -134,6 +143,28 @@ plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_ou
  * [begin, end) that `rank` of `world` owns (what psi_r_shard processes). */
 int64_t plugin_num_tiles(int64_t n);
 void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
+
+/* ---- the estimate the bandwidth is for ---- */
+
+/* Bytes of workspace kde_eval needs for n samples and m points (>= plugin_workspace_bytes(n)). */
+size_t kde_workspace_bytes(int64_t n, int64_t m);
+
+/*
+ * kde_eval: the kernel density estimator of Eq. 1 with the Gaussian kernel of
+ * Eq. 2 at m points:
+ *     d_f[k] = f(x_k, h) = (1/(n h)) sum_{i=1..n} K((x_k - X_i)/h),   K(u) = e^{-u^2/2}/sqrt(2 pi)
+ *   d_x      : device float32[n], n >= 1, not modified
+ *   d_points : device float32[m], m >= 0, any order (sorted or clustered points are
+ *              faster: each block of 1024 points only reads the samples that can reach it)
+ *   d_f      : device double[m], written
+ *   h        : finite, 1e-18 <= h <= 1e18 (else PLUGIN_E_INVALID)
+ * Each term is evaluated in fp32 (difference first) with MUFU.EX2; terms whose exponent is
+ * below -126.5 are exactly zero in that arithmetic and are not visited.  Accumulation is
+ * fp32 over 64 terms, then fp64, in a fixed order (bit-reproducible).  A non-finite sample
+ * makes every d_f[k] NaN; a NaN point gives NaN at that point.  Asynchronous on `stream`.
+ */
+plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_points, int64_t m,
+                       double* d_f, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Text of the last non-OK return on this thread ("" if none).  Static storage. */
 const char* plugin_last_error(void);

@@ -115,7 +115,14 @@ const char* plugin_last_error(void) { return g_err; }
 const char* plugin_version(void) { return "libplugin 0.1 sm_100a (psi: f32x2 + MUFU.EX2, dithered; fx128 accumulation)"; }
 
 plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  return plugin_h_ex(d_x, n, d_out, 0u, d_ws, ws_bytes, stream);
+}
+
+plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, unsigned int flags, void* d_ws,
+                          size_t ws_bytes, void* stream) {
   g_err[0] = 0;
+  if (flags & ~(unsigned int)PLUGIN_SKIP_UNDERFLOW) return fail(PLUGIN_E_INVALID, "unknown flags%s");
+  const int skip = (flags & PLUGIN_SKIP_UNDERFLOW) ? kPsiSkipUnderflow : 0;
   if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   plugin_status st = check_n(n, 2);
   if (st != PLUGIN_OK) return st;
@@ -125,10 +132,12 @@ plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out, void* 
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
   const int64_t tiles = psi_tiles(n);
   cudaError_t e;
-  if ((e = launch_psi(w.xs, n, 6, 0, 0.0, d_out, w.ctrl, 0, 0, tiles, s)) != cudaSuccess) return cuda_fail(e, "psi6");
+  if ((e = launch_psi(w.xs, n, 6, 0 | skip, 0.0, d_out, w.ctrl, 0, 0, tiles, s)) != cudaSuccess)
+    return cuda_fail(e, "psi6");
   if ((e = launch_finalize(0, w.ctrl, 0, nullptr, d_out, n, 0.0, 6, nullptr, nullptr, s)) != cudaSuccess)
     return cuda_fail(e, "finalize psi6");
-  if ((e = launch_psi(w.xs, n, 4, 1, 0.0, d_out, w.ctrl, 1, 0, tiles, s)) != cudaSuccess) return cuda_fail(e, "psi4");
+  if ((e = launch_psi(w.xs, n, 4, 1 | skip, 0.0, d_out, w.ctrl, 1, 0, tiles, s)) != cudaSuccess)
+    return cuda_fail(e, "psi4");
   if ((e = launch_finalize(1, w.ctrl, 1, nullptr, d_out, n, 0.0, 4, nullptr, nullptr, s)) != cudaSuccess)
     return cuda_fail(e, "finalize psi4");
   return PLUGIN_OK;
@@ -243,6 +252,38 @@ plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_ou
 }
 plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
   return after(1, d_total, d_out, stream);
+}
+
+size_t kde_workspace_bytes(int64_t n, int64_t m) {
+  if (n < 1) n = 1;
+  if (m < 0) m = 0;
+  return layout(n).total + kde_extra_bytes(n, m);
+}
+
+plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_points, int64_t m, double* d_f,
+                       void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  if (m < 0 || m > kMaxN) return fail(PLUGIN_E_INVALID, "m out of range%s (m=%lld)", "", (long long)m);
+  if (!d_x || (m > 0 && (!d_points || !d_f))) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  // h must be finite, > 0 and keep -log2(e)/(2 h^2) a normal float32
+  if (!(std::isfinite(h) && h >= 1e-18 && h <= 1e18)) return fail(PLUGIN_E_INVALID, "h must be in [1e-18, 1e18]%s");
+  if (m == 0) return PLUGIN_OK;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  if (ws_bytes < kde_workspace_bytes(n, m))
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)kde_workspace_bytes(n, m));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
+  if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
+  // Step I reduction only for its non-finite flag (a NaN/Inf sample makes every f NaN)
+  plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
+  if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  void* extra = static_cast<char*>(d_ws) + w.L.total;
+  if ((e = launch_kde(w.xs, n, h, d_points, m, w.ctrl, extra, d_f, s)) != cudaSuccess) return cuda_fail(e, "kde");
+  return PLUGIN_OK;
 }
 
 }  // extern "C"

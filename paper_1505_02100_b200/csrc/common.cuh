@@ -57,7 +57,8 @@ cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials
 cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
                         int64_t nblocks, cudaStream_t s);
 // mode: 0 = plugin pass r=6 (g from out->g1), 1 = plugin pass r=4 (g from out->g2),
-//       2 = psi_r with host g
+//       2 = psi_r with host g; | kPsiSkipUnderflow: skip tiles whose terms are all exactly 0
+constexpr int kPsiSkipUnderflow = 4;
 cudaError_t launch_psi(const float* xs, int64_t n, int r, int mode, double g_host, const plugin_result* out,
                        Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, cudaStream_t s);
 // what: 0 = plugin r=6 finalize, 1 = plugin r=4 finalize, 2 = psi_r -> d_psi, 3 = export limbs
@@ -65,5 +66,11 @@ cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* 
                             int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
                             cudaStream_t s);
 cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
+// KDE of Eq. 1-2 at m points over the sorted sample xs (kde.cu); `extra` holds
+// kde_extra_bytes(n, m) bytes of workspace
+size_t kde_extra_bytes(int64_t n, int64_t m);
+int kde_segments(int64_t n, int64_t m);
+cudaError_t launch_kde(const float* xs, int64_t n, double h, const float* pts, int64_t m, const Ctrl* ctrl,
+                       void* extra, double* f, cudaStream_t s);
 
 }  // namespace plg

@@ -26,10 +26,9 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "simd.cuh"
 
 namespace plg {
-
-typedef unsigned long long u64;
 
 // fp32 chunk length (j per flush to fp64) and unroll of the j loop; -D overrides are tuning only
 #ifndef PSI_CH
@@ -39,40 +38,6 @@ typedef unsigned long long u64;
 #define PSI_UNROLL 16
 #endif
 constexpr int kPsiUnroll = PSI_UNROLL;
-
-__device__ __forceinline__ u64 pk2(float a, float b) {
-  u64 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void upk2(u64 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-  u64 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ float ex2(float a) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
-  return r;
-}
 
 // packed constants {v, v}
 #define PK(v) ((((u64)__float_as_uint(v)) << 32) | (u64)__float_as_uint(v))
@@ -116,20 +81,6 @@ __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, 
   acc = fma2(p, e, acc);
 }
 
-// float -> double on the integer (ALU) pipe.  cvt.f64.f32 (F2F) issues on the XU pipe,
-// which MUFU.EX2 saturates; fp32 denormals and zero map to +-0, Inf/NaN are not expected
-// (non-finite samples are rejected before the pass).
-__device__ __forceinline__ double f32_to_f64_alu(float f) {
-  const unsigned int b = __float_as_uint(f);
-  const unsigned int mag = b & 0x7fffffffu;
-  unsigned int hi = ((mag >> 3) + 0x38000000u) | (b & 0x80000000u);
-  unsigned int lo = b << 29;
-  const bool tiny = mag < 0x00800000u;
-  hi = tiny ? (b & 0x80000000u) : hi;
-  lo = tiny ? 0u : lo;
-  return __hiloint2double((int)hi, (int)lo);
-}
-
 __device__ __forceinline__ Fx128 fx_from_double(double x) {
   Fx128 r;
   double fl = floor(x);
@@ -170,6 +121,9 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, con
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
 
+  // mode bit 2: skip tiles whose every term is exactly zero in fp32
+  const bool skip = (mode & kPsiSkipUnderflow) != 0;
+  mode &= 3;
   double g = g_host;
   if (mode == 0 || mode == 1) {
     if (out->status != PLUGIN_OK) return;
@@ -189,6 +143,17 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, con
     int64_t bi, bj;
     tile_coords(t, nb, bi, bj);
     const int64_t i0 = bi * T, j0 = bj * T;
+    if (skip && bi != bj) {
+      // sorted sample: the smallest |x_j - x_i| of an off-diagonal tile is xs[j0] - xs[i0 + T - 1];
+      // if even that gives |u| > 13.25 (with a 1e-5 margin for the per-row scale dither and fp32
+      // rounding), every exponent a = t c + p_i is below -127 and ex2.approx.ftz returns +0
+      // exactly, so the tile adds exactly nothing (bit-identical to evaluating it)
+      const double gap = (double)__ldg(xs + j0) - (double)__ldg(xs + i0 + T - 1);
+      if (gap * (double)s * (1.0 - 1e-5) > 13.25) {
+        __syncthreads();  // every thread has read s_tile before thread 0 overwrites it
+        continue;
+      }
+    }
     const int jcount = (int)((n - j0) < T ? (n - j0) : T);
     // stage the tile's j values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
     if (jcount == T) {

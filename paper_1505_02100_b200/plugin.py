@@ -55,6 +55,7 @@ def lib():
             "plugin_workspace_bytes": (sz, [i64]),
             "plugin_host_workspace_bytes": (sz, [i64]),
             "plugin_h": (i32, [P, i64, P, P, sz, P]),
+            "plugin_h_ex": (i32, [P, i64, P, ctypes.c_uint, P, sz, P]),
             "plugin_h_sync": (i32, [P, i64, P, P, sz, P]),
             "plugin_h_host": (i32, [P, i64, P, P, sz, P]),
             "psi_r": (i32, [P, i64, d, i32, P, P, sz, P]),
@@ -64,6 +65,8 @@ def lib():
             "plugin_after_psi4": (i32, [P, P, P]),
             "plugin_num_tiles": (i64, [i64]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "kde_workspace_bytes": (sz, [i64, i64]),
+            "kde_eval": (i32, [P, i64, d, P, i64, P, P, sz, P]),
             "plugin_last_error": (ctypes.c_char_p, []),
             "plugin_version": (ctypes.c_char_p, []),
         }
@@ -75,9 +78,11 @@ def lib():
     return _lib
 
 
-EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_sync", "plugin_h_host",
+PLUGIN_SKIP_UNDERFLOW = 1
+
+EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_last_error", "plugin_version")
+            "plugin_shard_tiles", "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
 
 
 def _check(st: int):
@@ -126,13 +131,16 @@ def read_result(buf: torch.Tensor) -> dict:
     return plugin_result.from_buffer_copy(h).to_dict()
 
 
-def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
-    """Alg. 1 on the device (asynchronous).  Returns the device result buffer."""
+def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
+             flags: int = 0):
+    """Alg. 1 on the device (asynchronous).  Returns the device result buffer.
+    ``flags``: PLUGIN_SKIP_UNDERFLOW (bit-identical result, less work; plugin_h_ex)."""
     x = _x(x)
     n = x.numel()
     ws = workspace(n, x.device) if ws is None else ws
     out = new_result(x.device) if out is None else out
-    _check(lib().plugin_h(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    _check(lib().plugin_h_ex(x.data_ptr(), n, out.data_ptr(), int(flags), ws.data_ptr(), ws.numel(),
+                             _stream(stream)))
     return out
 
 
@@ -204,6 +212,30 @@ def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
     lib().plugin_shard_tiles(n, rank, world, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+def kde_workspace_bytes(n: int, m: int) -> int:
+    return lib().kde_workspace_bytes(n, m)
+
+
+def kde_workspace(n: int, m: int, device=None) -> torch.Tensor:
+    nbytes = kde_workspace_bytes(n, m)
+    t = torch.empty(nbytes + 256, dtype=torch.uint8, device=device or "cuda")
+    off = (-t.data_ptr()) % 256
+    return t[off:off + nbytes]
+
+
+def kde_eval(x: torch.Tensor, h: float, points: torch.Tensor, out: torch.Tensor | None = None,
+             ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """f(x_k, h) of Eq. 1-2 at every point (device float64[m], asynchronous)."""
+    x = _x(x)
+    points = _x(points)
+    n, m = x.numel(), points.numel()
+    ws = kde_workspace(n, m, x.device) if ws is None else ws
+    out = torch.empty(m, dtype=torch.float64, device=x.device) if out is None else out
+    _check(lib().kde_eval(x.data_ptr(), n, float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(),
+                          ws.numel(), _stream(stream)))
+    return out
 
 
 def plugin_last_error() -> str:

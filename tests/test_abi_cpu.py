@@ -22,7 +22,7 @@ def L():
 def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(plugin_\w+|psi_r\w*)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(plugin_\w+|psi_r\w*|kde_\w+)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():
@@ -65,3 +65,15 @@ def test_tiles_cover_triangle(L, n):
         sizes = [e - b for b, e in spans]
         assert max(sizes) - min(sizes) <= 1           # equal-work tiles, balanced to one tile
     assert L.plugin_shard_tiles(n, 3, 2) == (0, 0)    # invalid rank -> empty range
+
+
+def test_kde_workspace_sizing(L):
+    # the psi workspace (sorted copy of X) plus per-(block, segment) fp64 partials, bounded by
+    # (8 * 148 target CTAs + one per point block) x 1024 points x 8 bytes
+    for n in (1, 1000, 1 << 20):
+        base = L.plugin_workspace_bytes(n)
+        for m in (0, 1, 1024, 65536, 1 << 22):
+            b = L.kde_workspace_bytes(n, m)
+            assert b >= base and b % 256 == 0
+            nb = -(-m // 1024)
+            assert b <= base + 8 * 1024 * (8 * 148 + nb) + 4 * nb + 512

@@ -241,3 +241,27 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
                 if lo <= hi:                # off-diagonal tiles: weight 2
                     ref += 2.0 * oracle_mod.psi_block_sum(zs, g, r, *rows, lo * T, min(n, hi * T + T))
             assert rel(got, ref) < TOL, (k, r, rank, got, ref, rel(got, ref))
+
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_skip_underflow_tiles_bit_identical(P, k):
+    # tiles whose every term is exactly 0 in fp32 are skipped; the
+    # result must be bit-identical to the full evaluation (every field, both passes)
+    x = torch.from_numpy(inputs.config_data(k)).cuda()
+    ws = P.workspace(x.numel(), x.device)
+    a = P.read_result(P.plugin_h(x, ws=ws))
+    b = P.read_result(P.plugin_h(x, ws=ws, flags=P.PLUGIN_SKIP_UNDERFLOW))
+    for key in a:
+        assert a[key] == b[key] or (math.isnan(a[key]) and math.isnan(b[key])), (key, a[key], b[key])
+
+
+def test_skip_underflow_far_clusters_bit_identical(P):
+    # two clusters 1e3 bandwidths apart: almost every off-diagonal tile is skipped
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.normal(0, 1, 30000), rng.normal(400, 1, 30000)]).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    a = P.read_result(P.plugin_h(xt))
+    b = P.read_result(P.plugin_h(xt, flags=P.PLUGIN_SKIP_UNDERFLOW))
+    assert a["status"] == 0 and all(a[k] == b[k] for k in a if not (isinstance(a[k], float) and math.isnan(a[k])))
+    with pytest.raises(P.PluginError):
+        P.plugin_h(xt, flags=8)
