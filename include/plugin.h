@@ -82,8 +82,9 @@ size_t plugin_workspace_bytes(int64_t n);
  * plugin_h: the whole Algorithm 1 on the device, asynchronously on `stream`.
  *   d_x   : device float32[n], n >= 2 (Step I divides by n-1; reading s9 of DESIGN.md)
  *   d_out : device plugin_result, written when the stream reaches the end of the call
- * Launches: Step I reduction, a sort of X into the workspace (summation order only),
- * the Step IV pass, its finalize (psi6, g2), the Step VI pass, its finalize (psi4, h).
+ * Launches: a sort of X into the workspace (summation order only), the Step I reduction,
+ * the Step IV pass, its finalize (psi6, g2), the Step VI pass, its finalize (psi4, h);
+ * for n <= 4096 all of it is one cooperative launch with the same results (plugin_h_ex).
  */
 plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
                        void* d_ws, size_t ws_bytes, void* stream);
@@ -94,6 +95,10 @@ plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
  * result is bit-identical to plugin_h; only the work changes (the
  * headline pair rate is always measured without it).  Unknown bits -> PLUGIN_E_INVALID. */
 #define PLUGIN_SKIP_UNDERFLOW 1u
+/* PLUGIN_MULTI_KERNEL: for n <= 4096 plugin_h runs the whole algorithm in one cooperative
+ * launch (sort, Step I, both passes and the scalar steps; bit-identical to the multi-kernel
+ * sequence); this flag forces the multi-kernel sequence instead (testing, timing). */
+#define PLUGIN_MULTI_KERNEL 2u
 plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, unsigned int flags,
                           void* d_ws, size_t ws_bytes, void* stream);
 

@@ -39,6 +39,8 @@ Layout layout(int64_t n) {
   off = align_up(off + sizeof(unsigned int) * 256 * (size_t)L.sort_blocks, 256);
   L.result = off;
   off = align_up(off + sizeof(plugin_result), 256);
+  L.fused = off;
+  off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid, 256);  // fused.cu partials (32 KB)
   L.total = off;
   return L;
 }
@@ -121,7 +123,7 @@ plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out, void* 
 plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, unsigned int flags, void* d_ws,
                           size_t ws_bytes, void* stream) {
   g_err[0] = 0;
-  if (flags & ~(unsigned int)PLUGIN_SKIP_UNDERFLOW) return fail(PLUGIN_E_INVALID, "unknown flags%s");
+  if (flags & ~(unsigned int)(PLUGIN_SKIP_UNDERFLOW | PLUGIN_MULTI_KERNEL)) return fail(PLUGIN_E_INVALID, "unknown flags%s");
   const int skip = (flags & PLUGIN_SKIP_UNDERFLOW) ? kPsiSkipUnderflow : 0;
   if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   plugin_status st = check_n(n, 2);
@@ -129,9 +131,17 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
   WS w;
   if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (n <= kFusedMaxN && !(flags & PLUGIN_MULTI_KERNEL)) {
+    // small n: the whole algorithm in one cooperative launch (fused.cu), bit-identical
+    Fx128* parts = reinterpret_cast<Fx128*>(static_cast<char*>(d_ws) + w.L.fused);
+    e = launch_fused(d_x, n, skip != 0, d_out, parts, s);
+    if (e == cudaSuccess) return PLUGIN_OK;
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "fused plugin");
+    (void)cudaGetLastError();  // not applicable here: take the multi-kernel path
+  }
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
   const int64_t tiles = psi_tiles(n);
-  cudaError_t e;
   if ((e = launch_psi(w.xs, n, 6, 0 | skip, 0.0, d_out, w.ctrl, 0, 0, tiles, s)) != cudaSuccess)
     return cuda_fail(e, "psi6");
   if ((e = launch_finalize(0, w.ctrl, 0, nullptr, d_out, n, 0.0, 6, nullptr, nullptr, s)) != cudaSuccess)

@@ -23,12 +23,27 @@ constexpr int kPsiThreads = 256;   // threads per CTA of the psi pass
 constexpr int kSortTile = 4096;    // keys per CTA in the radix sort
 constexpr int kSortThreads = 256;
 constexpr int kStep1Blocks = 592;  // 4 x 148: fixed grid so Step I is deterministic
+// Step I grid for n samples (a function of n only: the reduction tree, hence the result, is fixed)
+inline __host__ __device__ int step1_grid(int64_t n) {
+  const int64_t want = (n + 2047) / 2048;
+  return (int)(want < kStep1Blocks ? (want < 1 ? 1 : want) : kStep1Blocks);
+}
+// the fused single-launch path (fused.cu) handles n up to this
+constexpr int64_t kFusedMaxN = 4096;
 
 // rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
 int psi_rows_per_thread(int64_t n);
 inline int64_t psi_tile_edge(int64_t n) { return (int64_t)kPsiThreads * psi_rows_per_thread(n); }
 inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
+
+// order-preserving float bits <-> uint32 radix key (sort.cu, fused.cu)
+__device__ __forceinline__ unsigned int bits2key(unsigned int b) {
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ unsigned int key2bits(unsigned int k) {
+  return (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+}
 
 // ---- signed 128-bit fixed point, value = hi + lo * 2^-64 ------------------------
 struct Fx128 { unsigned long long lo; long long hi; };
@@ -44,7 +59,7 @@ struct Ctrl {                       // zeroed at the start of every API call
 static_assert(sizeof(Ctrl) <= 512, "ctrl block");
 
 struct Layout {
-  size_t ctrl, step1, xs, tmp, hist, result, total;
+  size_t ctrl, step1, xs, tmp, hist, result, fused, total;
   int64_t sort_blocks;
 };
 Layout layout(int64_t n);
@@ -66,6 +81,10 @@ cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* 
                             int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
                             cudaStream_t s);
 cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
+// the whole of Alg. 1 in one cooperative launch for n <= kFusedMaxN (fused.cu); parts holds
+// 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
+constexpr int kFusedMaxGrid = 1024;
+cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s);
 // KDE of Eq. 1-2 at m points over the sorted sample xs (kde.cu); `extra` holds
 // kde_extra_bytes(n, m) bytes of workspace
 size_t kde_extra_bytes(int64_t n, int64_t m);

@@ -1,0 +1,154 @@
+// fused.cu -- the whole of Algorithm 1 in ONE cooperative launch for
+// small samples (n <= kFusedMaxN = 4096, which covers the paper's own workloads n = 128..1024
+// of Tables 2-4 and BASELINE config 1).  At these sizes a pass is ~0.1-4 us of arithmetic, so
+// the 20 launches of the multi-kernel path dominate; here they become one launch and two
+// grid-wide barriers.
+//
+// Every CTA loads X into shared memory, sorts it (bitonic sort on the radix keys of sort.cu:
+// the same unique ascending array), and computes Step I and Steps II-III redundantly with the
+// reduction tree of step1_kernel (steps.cuh), so every CTA holds the same g1 without
+// communication.  The psi pass tiles (psi_tile.cuh, T = 256) are dealt round-robin to the
+// CTAs; each CTA writes its exact 128-bit fixed-point partial to its own slot, the grid
+// synchronises, and every CTA adds the slots (integer addition: order-free) and finalises
+// Step V identically; the Step VI pass follows the same way and CTA 0 writes the result.
+// Every tile sum, the fixed-point total and the scalar chain are computed by the same device
+// code as the multi-kernel path, so the result is bit-identical to it (tested).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "psi_tile.cuh"
+#include "steps.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace plg {
+
+// ascending bitonic sort of npad (a power of two) keys in shared memory, whole CTA
+__device__ __forceinline__ void cta_bitonic_sort(unsigned int* key, int npad) {
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (npad >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (j - 1));  // lower index of the i-th pair at stride j
+        const int hi = lo + j;
+        const bool asc = (lo & k) == 0;
+        const unsigned int a = key[lo], b = key[hi];
+        if ((a > b) == asc) { key[lo] = b; key[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ Fx128 ldcg_fx(const Fx128* p) {
+  Fx128 r;
+  r.lo = __ldcg(&p->lo);
+  r.hi = __ldcg(&p->hi);
+  return r;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kPsiThreads)
+plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, int skip, plugin_result* out,
+                    Fx128* parts) {
+  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded
+  __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
+  __shared__ int sh_bad[8];
+  __shared__ double p1[2 * 8];
+  __shared__ plugin_result res;
+  constexpr int T = kPsiThreads * R;
+  unsigned int* key = reinterpret_cast<unsigned int*>(xsm);
+  const int tid = threadIdx.x;
+
+  // sort (keys of the raw bits: pads are 0xffffffff and sort last)
+  for (int i = tid; i < npad; i += kPsiThreads)
+    key[i] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
+  __syncthreads();
+  cta_bitonic_sort(key, npad);
+  for (int i = tid; i < n; i += kPsiThreads) key[i] = key2bits(key[i]);
+  __syncthreads();
+  const float xpad = xsm[n - 1];
+  for (int64_t i = n + tid; i < nsx; i += kPsiThreads) xsm[i] = xpad;
+  if (tid == 0) init_result(&res, n);
+  __syncthreads();
+
+  // Step I (+ II, III) with step1_kernel's reduction tree over step1_grid(n) blocks
+  const int nb1 = step1_grid(n);
+  const double K = (double)xsm[0];
+  int bad = 0;
+  for (int b = 0; b < nb1; ++b) {
+    double a, q;
+    int bb;
+    step1_block(xsm, n, K, b, nb1, sh1, sh2, sh_bad, a, q, bb);
+    if (tid == 0) { p1[2 * b] = a; p1[2 * b + 1] = q; bad |= bb; }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double a, q;
+    step1_total<false>(p1, nb1, a, q);
+    if (tid == 0) step1_epilogue(a, q, n, K, bad != 0, &res);
+  }
+  __syncthreads();
+
+  // Steps IV/V and VI/VII
+  cg::grid_group grid = cg::this_grid();
+  const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool ok = res.status == PLUGIN_OK;  // the same in every CTA
+    if (ok) {
+      const float s = __double2float_rn(1.0 / (pass == 0 ? res.g1 : res.g2));
+      Fx128 acc = {0ull, 0ll};
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t bi, bj;
+        tile_coords(t, nb, bi, bj);
+        const int64_t i0 = bi * T, j0 = bj * T;
+        if (skip && bi != bj &&
+            ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > 13.25)
+          continue;  // all terms exactly zero (psi.cu); uniform across the CTA
+        const int jcount = (int)((n - j0) < T ? (n - j0) : T);
+        const double w = (bi == bj) ? 1.0 : 2.0;
+        const double tt = (pass == 0) ? psi_tile_sum<R, 6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
+                                      : psi_tile_sum<R, 4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
+        if (tid == 0) fx_add(acc, fx_from_double(tt));
+      }
+      if (tid == 0) parts[pass * gridDim.x + blockIdx.x] = acc;
+    }
+    grid.sync();
+    if (ok) {
+      if (tid == 0) {
+        Fx128 tot = {0ull, 0ll};
+        for (unsigned int b = 0; b < gridDim.x; ++b) fx_add(tot, ldcg_fx(parts + pass * gridDim.x + b));
+        finalize_pass(pass, fx_to_double(tot), n, &res);
+      }
+      __syncthreads();
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) *out = res;
+}
+
+cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {
+  if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n) != 1) return cudaErrorNotSupported;
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    int dev = 0, sms = 0, occ = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<1>, kPsiThreads,
+                                                  sizeof(float) * kFusedMaxN);
+    max_grid = coop ? sms * occ : 0;
+    if (max_grid > kFusedMaxGrid) max_grid = kFusedMaxGrid;
+  }
+  if (max_grid <= 0) return cudaErrorNotSupported;
+  int npad = 2;
+  while (npad < n) npad <<= 1;
+  const int64_t T = kPsiThreads, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
+  int nsx = (int)(nb * T > npad ? nb * T : npad);
+  int grid = (int)(tiles < max_grid ? tiles : max_grid);
+  size_t smem = sizeof(float) * (size_t)nsx;
+  void* args[] = {(void*)&x, (void*)&n, (void*)&npad, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)plugin_fused_kernel<1>, dim3(grid), dim3(kPsiThreads),
+                                              args, smem, s);
+  return e;
+}
+
+}  // namespace plg

@@ -1,0 +1,179 @@
+// psi_tile.cuh -- one T x T tile (T = 256 R) of the pair triangle of Steps IV/VI
+// (Eq. 5-7), shared by the persistent pass kernel (psi.cu) and the fused
+// small-n kernel (fused.cu) so both give bit-identical tile sums.  See psi.cu for the
+// arithmetic and DESIGN.md §6 for the numerics.  Product code: nothing here is shared
+// with oracle/.
+#pragma once
+#include "common.cuh"
+#include "simd.cuh"
+
+namespace plg {
+
+// fp32 chunk length (j per flush to fp64) and unroll of the j loop; -D overrides are tuning only
+#ifndef PSI_CH
+#define PSI_CH 64
+#endif
+#ifndef PSI_UNROLL
+#define PSI_UNROLL 16
+#endif
+constexpr int kPsiUnroll = PSI_UNROLL;
+
+// packed constants {v, v}
+#define PK(v) ((((u64)__float_as_uint(v)) << 32) | (u64)__float_as_uint(v))
+
+// per-row dither: phase p_i in (-2, -1] (exact fp32, 24 random bits) and scale offset k_i in [-7, 7]
+__device__ __forceinline__ unsigned int row_hash(int64_t i) { return (unsigned int)i * 2654435769u; }
+__device__ __forceinline__ float row_phase(int64_t i) {
+  return -1.0f - (float)(row_hash(i) >> 8) * (1.0f / 16777216.0f);
+}
+__device__ __forceinline__ int row_scale_offset(int64_t i) {
+  unsigned int h = ((unsigned int)i * 0x85EBCA6Bu) ^ 0x9E3779B9u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  return (int)(((h >> 16) * 15u) >> 16) - 7;
+}
+
+template <int ORDER, bool MASK>
+__device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, bool m0 = true, bool m1 = true) {
+  const u64 c2 = 0xBF38AA3BBF38AA3Bull;  // {fp32(-log2(e)/2)} x 2 = -0.72134752f
+  u64 d = sub2(xj, xi);
+  u64 u = mul2(d, s2);
+  u64 t = mul2(u, u);
+  u64 a = fma2(t, c2, ph);
+  float a0, a1;
+  upk2(a, a0, a1);
+  float e0 = ex2(a0), e1 = ex2(a1);
+  if (MASK) {
+    e0 = m0 ? e0 : 0.f;
+    e1 = m1 ? e1 : 0.f;
+  }
+  u64 e = pk2(e0, e1);
+  u64 p;
+  if (ORDER == 6) {
+    p = add2(t, 0xC1700000C1700000ull);      // t - 15
+    p = fma2(p, t, 0x4234000042340000ull);   // (t - 15) t + 45
+    p = fma2(p, t, 0xC1700000C1700000ull);   // ((t - 15) t + 45) t - 15
+  } else {
+    p = add2(t, 0xC0C00000C0C00000ull);      // t - 6
+    p = fma2(p, t, 0x4040000040400000ull);   // (t - 6) t + 3
+  }
+  acc = fma2(p, e, acc);
+}
+
+__device__ __forceinline__ Fx128 fx_from_double(double x) {
+  Fx128 r;
+  double fl = floor(x);
+  r.hi = (long long)fl;
+  double fr = x - fl;  // exact, in [0, 1)
+  r.lo = __double2ull_rn(fr * 18446744073709551616.0);
+  return r;
+}
+__device__ __forceinline__ void fx_add(Fx128& a, Fx128 b) {
+  unsigned long long lo = a.lo + b.lo;
+  a.hi += b.hi + (lo < a.lo ? 1 : 0);
+  a.lo = lo;
+}
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, int64_t& bj) {
+  // row-major upper triangle incl. diagonal: row b starts at off(b) = b*nb - b(b-1)/2
+  double A = 2.0 * (double)nb + 1.0;
+  int64_t b = (int64_t)((A - sqrt(A * A - 8.0 * (double)t)) * 0.5);
+  if (b < 0) b = 0;
+  if (b > nb - 1) b = nb - 1;
+  while (b > 0 && b * nb - b * (b - 1) / 2 > t) --b;
+  while (b + 1 < nb && (b + 1) * nb - (b + 1) * b / 2 <= t) ++b;
+  bi = b;
+  bj = b + (t - (b * nb - b * (b - 1) / 2));
+}
+
+// The weighted sum (w = 2 off-diagonal, 1 diagonal) of one tile, divided by phi(0).
+//   sx    : the tile's j values (jcount of them, then padding up to a multiple of PSI_CH with
+//           xpad), 16-byte aligned, visible to all threads (shared memory)
+//   xrows : the sorted sample, rows i0 .. i0 + T - 1 (i >= n reads as xpad and is dropped)
+//   red   : shared scratch of kPsiThreads / 32 doubles
+// Called by all 256 threads; the result is valid in thread 0.  Contains __syncthreads().
+template <int R, int ORDER, bool LDG>
+__device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __restrict__ xrows, int64_t n, int64_t i0,
+                                               int jcount, float s, float xpad, double w, double* red) {
+  constexpr int CH = PSI_CH;  // j per fp32 chunk (CH/2 per packed lane) before the fp64 flush
+  const int tid = threadIdx.x;
+  u64 xi[R], ph[R], s2[R];
+  double drow[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = i0 + k * kPsiThreads + tid;
+    const float v = (i < n) ? (LDG ? __ldg(xrows + i) : xrows[i]) : xpad;
+    xi[k] = pk2(v, v);
+    const float p = row_phase(i);
+    ph[k] = pk2(p, p);
+    const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+    s2[k] = pk2(si, si);
+    drow[k] = 0.0;
+  }
+  __syncthreads();
+  const float4* sx4 = reinterpret_cast<const float4*>(sx);
+  const int full = jcount / CH;
+  for (int c = 0; c < full; ++c) {
+    u64 acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0ull;
+#pragma unroll kPsiUnroll
+    for (int q = 0; q < CH / 4; ++q) {
+      const float4 v = sx4[c * (CH / 4) + q];
+      const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        pair2<ORDER, false>(j01, xi[k], s2[k], ph[k], acc[k]);
+        pair2<ORDER, false>(j23, xi[k], s2[k], ph[k], acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      float a0, a1;
+      upk2(acc[k], a0, a1);
+      drow[k] += f32_to_f64_alu(a0 + a1);
+    }
+  }
+  if (full * CH < jcount) {  // ragged last chunk of the last column tile
+    u64 acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0ull;
+    const int jb = full * CH;
+    for (int q = 0; q < CH / 4; ++q) {
+      const float4 v = sx4[full * (CH / 4) + q];
+      const int j = jb + 4 * q;
+      const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        pair2<ORDER, true>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
+        pair2<ORDER, true>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      float a0, a1;
+      upk2(acc[k], a0, a1);
+      drow[k] += f32_to_f64_alu(a0 + a1);
+    }
+  }
+  // undo the dither per row, drop padding rows, weight the tile
+  double tsum = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = i0 + k * kPsiThreads + tid;
+    const double comp = exp2(-(double)row_phase(i));
+    if (i < n) tsum = fma(drow[k], comp, tsum);
+  }
+  tsum *= w;
+  for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+  if ((tid & 31) == 0) red[tid >> 5] = tsum;
+  __syncthreads();
+  double tt = 0.0;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < kPsiThreads / 32; ++k) tt += red[k];
+  }
+  return tt;
+}
+
+}  // namespace plg

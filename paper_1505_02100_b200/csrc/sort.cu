@@ -12,15 +12,9 @@
 
 namespace plg {
 
-// Order-preserving float -> uint32 key, on the raw bits (loaded as integers: written on
-// floats, nvcc turns `bits | 0x80000000` into an FADD -|x| that canonicalises NaN payloads).
-__device__ __forceinline__ unsigned int bits2key(unsigned int b) {
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ unsigned int key2bits(unsigned int k) {
-  return (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-}
-
+// Order-preserving float -> uint32 key (bits2key/key2bits in common.cuh), on the raw bits
+// (loaded as integers: written on floats, nvcc turns `bits | 0x80000000` into an FADD -|x|
+// that canonicalises NaN payloads).
 template <bool FIRST>
 __device__ __forceinline__ unsigned int load_key(const void* src, int64_t i) {
   const unsigned int v = __ldg(reinterpret_cast<const unsigned int*>(src) + i);

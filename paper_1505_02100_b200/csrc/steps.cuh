@@ -1,0 +1,130 @@
+// steps.cuh -- device code of the O(n) and O(1) steps of Algorithm 1,
+// shared by the multi-kernel path (scalar.cu) and the fused small-n kernel (fused.cu) so both
+// compute bit-identical results.  Product code: nothing here is shared with oracle/.
+#pragma once
+#include <cmath>
+
+#include "common.cuh"
+
+namespace plg {
+
+// x^k by repeated multiplication: keeps raw <-> z conversions exact under 2^k scaling.
+__device__ __forceinline__ double ipow(double b, int k) {
+  double r = 1.0;
+  for (int i = 0; i < k; ++i) r *= b;
+  return r;
+}
+
+// Step I, one block's share: V is shift invariant, so it is evaluated on
+// d_i = X_i - X_0 (exact in fp64) with the printed one-pass form; this block (index b of
+// nblocks, 256 threads) sums d and d^2 over i = b*256 + tid + k*nblocks*256.  Thread 0
+// returns the block partials (a = sum d, q = sum d^2) and the non-finite flag.
+__device__ __forceinline__ void step1_block(const float* x, int64_t n, double K, int b, int nblocks, double* sh1,
+                                            double* sh2, int* sh_bad, double& a, double& q, int& bb) {
+  double s1 = 0.0, s2 = 0.0;
+  int bad = 0;
+  for (int64_t i = (int64_t)b * 256 + threadIdx.x; i < n; i += (int64_t)nblocks * 256) {
+    const float v = x[i];
+    bad |= !isfinite(v);
+    const double d = (double)v - K;
+    s1 += d;
+    s2 = fma(d, d, s2);
+  }
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh1[w] = s1; sh2[w] = s2; sh_bad[w] = bad; }
+  __syncthreads();
+  a = 0.0; q = 0.0; bb = 0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) { a += sh1[k]; q += sh2[k]; bb |= sh_bad[k]; }
+  __syncthreads();  // sh* may be reused
+}
+
+// Step I, final: warp 0 adds the nblocks partials {a, q} (stride-2 array, in global memory
+// written by other blocks if GLOBAL, else in shared memory) in a fixed order.  Valid in lane 0.
+template <bool GLOBAL>
+__device__ __forceinline__ void step1_total(const double* partials, int nblocks, double& a, double& q) {
+  const int l = threadIdx.x & 31;
+  a = 0.0; q = 0.0;
+  for (int k = l; k < nblocks; k += 32) {
+    a += GLOBAL ? __ldcg(partials + 2 * k) : partials[2 * k];
+    q += GLOBAL ? __ldcg(partials + 2 * k + 1) : partials[2 * k + 1];
+  }
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+}
+
+// Step I result and Steps II-III from the totals; one thread.
+__device__ __forceinline__ void step1_epilogue(double a, double q, int64_t n, double K, bool nonfinite,
+                                               plugin_result* out) {
+  const double nd = (double)n;
+  const double var = (q - a * a / nd) / (nd - 1.0);
+  out->mean = K + a / nd;
+  out->var = var;
+  if (nonfinite) { out->status = PLUGIN_E_NONFINITE; return; }
+  if (!(var > 0.0)) { out->status = PLUGIN_E_DEGENERATE; return; }
+  const double sigma = sqrt(var);
+  out->sigma = sigma;
+  // Step II in z units (sigma_z = 1) and in data units
+  const double psi8_z = 105.0 / (32.0 * sqrt(kPi));
+  out->psi8_ns = psi8_z / ipow(sigma, 9);
+  // Step III
+  const double g1_z = pow(-2.0 * kK6at0 / (kMu2 * psi8_z * nd), 1.0 / 9.0);
+  out->g1_z = g1_z;
+  out->g1 = g1_z * sigma;
+}
+
+__device__ __forceinline__ double fx_to_double(Fx128 v) {
+  return (double)v.hi + (double)v.lo * 5.42101086242752217003726400434970855712890625e-20;  // 2^-64
+}
+
+// Step IV -> V (what = 0) or Step VI -> VII + Eq. 4 (what = 1) from the full double sum
+// S = sum_i sum_j K^(r)(u_ij) / phi(0); one thread.
+__device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plugin_result* out) {
+  if (out->status != PLUGIN_OK) return;
+  const double nd = (double)n;
+  const double sigma = out->sigma;
+  if (what == 0) {
+    // Step IV (Eq. 6) in z units: u = (z_i - z_j)/g1_z = (X_i - X_j)/g1
+    const double g1_z = out->g1_z;
+    const double psi6_z = kInvSqrt2Pi * S / (nd * nd * ipow(g1_z, 7));
+    out->S6 = S;
+    out->psi6_z = psi6_z;
+    out->psi6 = psi6_z / ipow(sigma, 7);
+    if (!(psi6_z < 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
+    // Step V
+    const double g2_z = pow(-2.0 * kK4at0 / (kMu2 * psi6_z * nd), 1.0 / 7.0);
+    out->g2_z = g2_z;
+    out->g2 = g2_z * sigma;
+  } else {
+    // Step VI (Eq. 7)
+    const double g2_z = out->g2_z;
+    const double psi4_z = kInvSqrt2Pi * S / (nd * nd * ipow(g2_z, 5));
+    out->S4 = S;
+    out->psi4_z = psi4_z;
+    out->psi4 = psi4_z / ipow(sigma, 5);
+    if (!(psi4_z > 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
+    // Step VII and Eq. 4
+    const double h_z = pow(kRK / (kMu2 * kMu2 * psi4_z * nd), 1.0 / 5.0);
+    out->h_z = h_z;
+    out->h = h_z * sigma;
+  }
+}
+
+__device__ __forceinline__ void init_result(plugin_result* out, int64_t n) {
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  out->status = PLUGIN_OK;
+  out->reserved = 0;
+  out->n = n;
+  double* f = &out->mean;
+  const int nf = (int)((sizeof(plugin_result) - offsetof(plugin_result, mean)) / sizeof(double));
+  for (int i = 0; i < nf; ++i) f[i] = qnan;
+}
+
+}  // namespace plg

@@ -79,6 +79,7 @@ def lib():
 
 
 PLUGIN_SKIP_UNDERFLOW = 1
+PLUGIN_MULTI_KERNEL = 2
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",

@@ -265,3 +265,45 @@ def test_skip_underflow_far_clusters_bit_identical(P):
     assert a["status"] == 0 and all(a[k] == b[k] for k in a if not (isinstance(a[k], float) and math.isnan(a[k])))
     with pytest.raises(P.PluginError):
         P.plugin_h(xt, flags=8)
+
+
+def _same(a, b):
+    return all(a[k] == b[k] or (isinstance(a[k], float) and math.isnan(a[k]) and math.isnan(b[k])) for k in a)
+
+
+@pytest.mark.parametrize("n", [2, 3, 31, 255, 256, 257, 1000, 1024, 1025, 2049, 4096])
+def test_fused_small_n_bit_identical_to_multi_kernel(P, oracle_mod, n):
+    # n <= 4096: plugin_h runs one cooperative launch (fused.cu); it must reproduce the
+    # multi-kernel sequence bit for bit, and both must match the oracle
+    x = inputs.mixture(n, 300 + n) if n > 3 else inputs.normal(n, 300 + n)
+    xt = torch.from_numpy(x).cuda()
+    ws = P.workspace(n, xt.device)
+    a = P.read_result(P.plugin_h(xt, ws=ws))
+    b = P.read_result(P.plugin_h(xt, ws=ws, flags=P.PLUGIN_MULTI_KERNEL))
+    c = P.read_result(P.plugin_h(xt, ws=ws, flags=P.PLUGIN_SKIP_UNDERFLOW))
+    assert _same(a, b) and _same(a, c), (a, b)
+    o = oracle_mod.plugin(x)
+    for key in ("psi6_z", "psi4_z", "h", "g1", "g2", "sigma"):
+        assert rel(a[key], o[key]) < TOL, (n, key, a[key], o[key])
+
+
+@pytest.mark.parametrize("case", ["constant", "nan", "inf"])
+def test_fused_error_status_matches_multi_kernel(P, case):
+    x = np.full(700, 1.25, np.float32)
+    if case != "constant":
+        x = inputs.normal(700, 1)
+        x[123] = np.nan if case == "nan" else np.inf
+    xt = torch.from_numpy(x).cuda()
+    a = P.read_result(P.plugin_h(xt))
+    b = P.read_result(P.plugin_h(xt, flags=P.PLUGIN_MULTI_KERNEL))
+    want = P.PLUGIN_E_DEGENERATE if case == "constant" else P.PLUGIN_E_NONFINITE
+    assert a["status"] == b["status"] == want
+    assert _same(a, b)
+
+
+def test_fused_toy_data_bit_identical(P):
+    x = torch.from_numpy(inputs.TOY.astype(np.float32)).cuda()
+    a = P.read_result(P.plugin_h(x))
+    b = P.read_result(P.plugin_h(x, flags=P.PLUGIN_MULTI_KERNEL))
+    assert _same(a, b)
+    assert rel(a["h"], 0.96146759322923324) < TOL   # SURVEY App. B.2 (50-digit value)
