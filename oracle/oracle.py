@@ -68,6 +68,8 @@ def lib():
             getattr(L, name).argtypes = [d]
         L.oracle_K.restype = d
         L.oracle_K.argtypes = [i32, d]
+        L.oracle_K_hermite.restype = d
+        L.oracle_K_hermite.argtypes = [i32, d]
         L.oracle_step1.restype = i32
         L.oracle_step1.argtypes = [P, i64, P]
         L.oracle_zscore.restype = None
@@ -97,8 +99,13 @@ def _f32(x) -> np.ndarray:
 
 
 def K(r: int, u: float) -> float:
-    """K^(r)(u) for r in {4, 6} (Alg. 1 Steps IV/VI)."""
+    """K^(r)(u): r in {4, 6} as printed in Alg. 1 Steps IV/VI; other even r by Hermite recurrence."""
     return lib().oracle_K(int(r), float(u))
+
+
+def K_hermite(r: int, u: float) -> float:
+    """K^(r)(u) = He_r(u) phi(u) by the Hermite recurrence, any even r >= 0."""
+    return lib().oracle_K_hermite(int(r), float(u))
 
 
 def phi(u: float) -> float:
@@ -238,10 +245,21 @@ def psi_halved_sum(z: np.ndarray, g: float, r: int, threads: int = 0, checkpoint
     return _neumaier(parts)
 
 
+def K_at_zero(r: int) -> float:
+    """K^(r)(0): the printed constants for r = 6, 4, else (-1)^(r/2) (r-1)!! phi(0)."""
+    if r == 6:
+        return K6_0
+    if r == 4:
+        return K4_0
+    dfact = 1.0
+    for k in range(r - 1, 0, -2):
+        dfact *= k
+    return (-1.0) ** (r // 2) * dfact / math.sqrt(2.0 * PI)
+
+
 def psi_from_halved_sum(T: float, n: int, g: float, r: int) -> float:
     """Eq. 6/7: Psi_r(g) = (2 T + n K^(r)(0)) / (n^2 g^(r+1))."""
-    k0 = K6_0 if r == 6 else K4_0
-    return (2.0 * T + n * k0) / (n * n * g ** (r + 1))
+    return (2.0 * T + n * K_at_zero(r)) / (n * n * g ** (r + 1))
 
 
 def psi(z, g: float, r: int, threads: int = 0, checkpoint: str | None = None, log=None) -> float:
@@ -265,6 +283,40 @@ def psi_literal(z, g: float, r: int) -> float:
     z = np.ascontiguousarray(z, dtype=np.float64)
     n = z.size
     return lib().oracle_psi_literal_sum(_ptr(z), n, float(g), int(r)) / (n * n * g ** (r + 1))
+
+
+# ---- the l-stage direct plug-in family of Alg. 1 ----------------
+def psi_ns(r: int, sigma: float) -> float:
+    """Normal-scale functional Psi_r^NS = (-1)^(r/2) r! / ((2 sigma)^(r+1) (r/2)! sqrt(pi))
+    (Wand & Jones; Step II, is r = 8)."""
+    return (-1.0) ** (r // 2) * math.factorial(r) / ((2.0 * sigma) ** (r + 1) * math.factorial(r // 2)
+                                                     * math.sqrt(PI))
+
+
+def dpi(x, stages: int, threads: int = 0) -> dict:
+    """l-stage direct plug-in (Alg. 1 is l = 2), z-score path (Eq. 3-4):
+    Psi_{2l+4} <- Psi^NS;  for j = l..1:  g_j = (-2 K^(2j+2)(0) / (mu2 Psi_{2j+4} n))^(1/(2j+5)),
+    Psi_{2j+2} <- Psi_hat_{2j+2}(g_j);  h = (R(K) / (mu2^2 Psi_4 n))^(1/5) sigma."""
+    x = _f32(x)
+    n = int(x.size)
+    s1 = step1(x)
+    sigma = s1["sigma"]
+    z = zscore(x, s1["mean"], sigma)
+    psi_next = psi_ns(2 * stages + 4, 1.0)
+    res = {"n": n, "stages": stages, "sigma": sigma, "psi_ns_z": psi_next, "g_z": {}, "psi_z": {}}
+    for j in range(stages, 0, -1):
+        r = 2 * j + 2
+        num = -2.0 * K_at_zero(r)
+        if not num / psi_next > 0.0:
+            raise OracleError("E_DOMAIN", f"stage {j}: Psi_{r + 2} = {psi_next!r} has the wrong sign")
+        g = (num / (MU2 * psi_next * n)) ** (1.0 / (r + 3))
+        psi_next = psi(z, g, r, threads)
+        res["g_z"][j] = g
+        res["psi_z"][j] = psi_next
+    h_z = h_bandwidth(psi_next, n)
+    res["h_z"] = h_z
+    res["h"] = h_z * sigma
+    return res
 
 
 # ---- Eq. 1-2: the kernel density estimate that h is for (SURVEY §8(f) NEXT 1) ----------

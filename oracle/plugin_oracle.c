@@ -53,11 +53,28 @@ double oracle_K4(double x) {
   return (x4 - 6.0 * x2 + 3.0) * exp(-0.5 * x2) / sqrt(2.0 * ORACLE_PI);
 }
 
-/* r in {4, 6}; anything else returns NaN. */
+/*
+ * K^(r)(x) = d^r/dx^r phi(x) for any even r >= 0 (the r-th derivative
+ * reading R1 of the kernels of Steps IV/VI):  phi^(r)(x) = (-1)^r He_r(x) phi(x) with the
+ * probabilists' Hermite polynomials He_0 = 1, He_1 = x, He_{k+1} = x He_k - k He_{k-1}.
+ */
+double oracle_K_hermite(int r, double x) {
+  if (r < 0 || (r & 1)) return NAN;
+  double hm1 = 1.0, h = x;  /* He_0, He_1 */
+  if (r == 0) return oracle_phi(x);
+  for (int k = 1; k < r; ++k) {
+    double hp1 = x * h - (double)k * hm1;
+    hm1 = h;
+    h = hp1;
+  }
+  return h * oracle_phi(x);
+}
+
+/* r = 6, 4: the printed polynomials of Steps IV/VI; other even r: the Hermite form above. */
 double oracle_K(int r, double x) {
   if (r == 6) return oracle_K6(x);
   if (r == 4) return oracle_K4(x);
-  return NAN;
+  return oracle_K_hermite(r, x);
 }
 
 /*
