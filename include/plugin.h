@@ -21,7 +21,7 @@
  *    plugin_workspace_bytes(n) bytes, 256-byte aligned, no initialisation needed;
  *    two calls may run concurrently only with distinct workspaces.
  *  - Return value (plugin_status): immediate errors only -- PLUGIN_E_INVALID for
- *    bad arguments (null pointer, n out of range, r not in {4,6}, g not finite
+ *    bad arguments (null pointer, n out of range, r not even in [0,12], g not finite
  *    and > 0, workspace too small, rank/world inconsistent) and PLUGIN_E_CUDA for
  *    a launch failure.  Data-dependent errors (non-finite sample, zero variance,
  *    psi6 >= 0, psi4 <= 0) are written by the device into plugin_result.status;
@@ -117,7 +117,8 @@ plugin_status plugin_h_host(const float* h_x, int64_t n, plugin_result* h_out,
                             void* d_ws, size_t ws_bytes, void* stream);
 
 /*
- * psi_r: Psi_r(g) of Steps IV/VI for a given bandwidth g (data units), r in {4,6}:
+ * psi_r: Psi_r(g) of Steps IV/VI for a given bandwidth g (data units), r in {4,6} (and any
+ * even r <= 12 with K^(r) = He_r(u) phi(u), the family of plugin_dpi):
  *   Psi_r(g) = (n^2 g^(r+1))^-1 sum_{i,j} K^(r)((x_i - x_j)/g), diagonal included,
  * evaluated as 2 sum_{i<j} + n K^(r)(0) (Eq. 6/7).  n >= 1, g finite > 0.
  * *d_psi (device double) is written; a non-finite sample makes it NaN.
@@ -148,6 +149,36 @@ plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_ou
  * [begin, end) that `rank` of `world` owns (what psi_r_shard processes). */
 int64_t plugin_num_tiles(int64_t n);
 void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
+
+/* ---- the l-stage direct plug-in family ---- */
+
+/*
+ * Algorithm 1 is the l = 2 member of the direct plug-in family of the book the paper follows
+ * ("the symbols used are exactly such as in the book"):
+ *     Psi_{2l+4} <- Psi^NS_{2l+4} = (-1)^(l+2) (2l+3)!! / (2^(l+3) sqrt(pi) sigma^(2l+5))
+ *     for j = l..1:  g_j = (-2 K^(2j+2)(0) / (mu2 Psi_{2j+4} n))^(1/(2j+5)),
+ *                    Psi_{2j+2} <- Psi_hat_{2j+2}(g_j)     (pair passes as Steps IV/VI)
+ *     h = (R(K) / (mu2^2 Psi_4 n))^(1/5)                    (Step VII, Eq. 4)
+ * l = 0 is the normal reference rule h = (4/(3n))^(1/5) sigma; l = 2 is plugin_h (bit-identical).
+ * Arrays are indexed by stage: [j-1] holds g_j and Psi_{2j+2}(g_j).
+ */
+#define PLUGIN_DPI_MAX_STAGES 5
+typedef struct {
+  int32_t status;     /* plugin_status of the data-dependent checks (as plugin_result)          */
+  int32_t stages;     /* l                                                                      */
+  int64_t n;
+  double mean, var, sigma;                 /* Step I                                             */
+  double psi_ns_z;                         /* Psi^NS_{2l+4}, z units (sigma_z = 1)              */
+  double g_z[PLUGIN_DPI_MAX_STAGES], g[PLUGIN_DPI_MAX_STAGES];       /* z and data units        */
+  double psi_z[PLUGIN_DPI_MAX_STAGES], psi[PLUGIN_DPI_MAX_STAGES];   /* z and data units        */
+  double h_z, h;
+} plugin_dpi_result;
+
+/* The l-stage direct plug-in bandwidth, 0 <= stages <= 5 (passes of order 2l+2 .. 4, each
+ * over the i<j triangle like Steps IV/VI); n >= 2; asynchronous; d_out on the device.
+ * Needs plugin_workspace_bytes(n).  Data errors in d_out->status as for plugin_h. */
+plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_result* d_out,
+                         void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- the estimate the bandwidth is for ---- */
 

@@ -124,7 +124,7 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
                           size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   if (flags & ~(unsigned int)(PLUGIN_SKIP_UNDERFLOW | PLUGIN_MULTI_KERNEL)) return fail(PLUGIN_E_INVALID, "unknown flags%s");
-  const int skip = (flags & PLUGIN_SKIP_UNDERFLOW) ? kPsiSkipUnderflow : 0;
+  const int skip = (flags & PLUGIN_SKIP_UNDERFLOW) ? 1 : 0;
   if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   plugin_status st = check_n(n, 2);
   if (st != PLUGIN_OK) return st;
@@ -135,18 +135,18 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
   if (n <= kFusedMaxN && !(flags & PLUGIN_MULTI_KERNEL)) {
     // small n: the whole algorithm in one cooperative launch (fused.cu), bit-identical
     Fx128* parts = reinterpret_cast<Fx128*>(static_cast<char*>(d_ws) + w.L.fused);
-    e = launch_fused(d_x, n, skip != 0, d_out, parts, s);
+    e = launch_fused(d_x, n, skip, d_out, parts, s);
     if (e == cudaSuccess) return PLUGIN_OK;
     if (e != cudaErrorNotSupported) return cuda_fail(e, "fused plugin");
     (void)cudaGetLastError();  // not applicable here: take the multi-kernel path
   }
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
   const int64_t tiles = psi_tiles(n);
-  if ((e = launch_psi(w.xs, n, 6, 0 | skip, 0.0, d_out, w.ctrl, 0, 0, tiles, s)) != cudaSuccess)
+  if ((e = launch_psi(w.xs, n, 6, skip, 0.0, &d_out->g1, &d_out->status, w.ctrl, 0, 0, tiles, s)) != cudaSuccess)
     return cuda_fail(e, "psi6");
   if ((e = launch_finalize(0, w.ctrl, 0, nullptr, d_out, n, 0.0, 6, nullptr, nullptr, s)) != cudaSuccess)
     return cuda_fail(e, "finalize psi6");
-  if ((e = launch_psi(w.xs, n, 4, 1 | skip, 0.0, d_out, w.ctrl, 1, 0, tiles, s)) != cudaSuccess)
+  if ((e = launch_psi(w.xs, n, 4, skip, 0.0, &d_out->g2, &d_out->status, w.ctrl, 1, 0, tiles, s)) != cudaSuccess)
     return cuda_fail(e, "psi4");
   if ((e = launch_finalize(1, w.ctrl, 1, nullptr, d_out, n, 0.0, 4, nullptr, nullptr, s)) != cudaSuccess)
     return cuda_fail(e, "finalize psi4");
@@ -198,7 +198,7 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
   if (!d_x || !d_psi) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   plugin_status st = check_n(n, 1);
   if (st != PLUGIN_OK) return st;
-  if (r != 4 && r != 6) return fail(PLUGIN_E_INVALID, "r must be 4 or 6%s (r=%lld)", "", r);
+  if (r < 0 || r > 12 || (r & 1)) return fail(PLUGIN_E_INVALID, "r must be even, 0..12%s (r=%lld)", "", r);
   if (!(std::isfinite(g) && g > 0.0)) return fail(PLUGIN_E_INVALID, "g must be finite and > 0%s");
   WS w;
   if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
@@ -209,7 +209,7 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
   // Step I reduction only for its non-finite flag (a NaN/Inf sample makes Psi NaN)
   plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
-  if ((e = launch_psi(w.xs, n, r, 2, g, nullptr, w.ctrl, 1, 0, psi_tiles(n), s)) != cudaSuccess)
+  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_tiles(n), s)) != cudaSuccess)
     return cuda_fail(e, "psi");
   if ((e = launch_finalize(2, w.ctrl, 1, nullptr, nullptr, n, g, r, d_psi, nullptr, s)) != cudaSuccess)
     return cuda_fail(e, "finalize");
@@ -241,7 +241,8 @@ plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_re
   plugin_shard_tiles(n, rank, world, &tb, &te);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int slot = (r == 6) ? 0 : 1;
-  cudaError_t e = launch_psi(w.xs, n, r, r == 6 ? 0 : 1, 0.0, d_out, w.ctrl, slot, tb, te, s);
+  cudaError_t e = launch_psi(w.xs, n, r, 0, 0.0, r == 6 ? &d_out->g1 : &d_out->g2, &d_out->status, w.ctrl, slot,
+                             tb, te, s);
   if (e != cudaSuccess) return cuda_fail(e, "psi shard");
   if ((e = launch_finalize(3, w.ctrl, slot, nullptr, nullptr, n, 0.0, r, nullptr, d_partial, s)) != cudaSuccess)
     return cuda_fail(e, "export partial");
@@ -262,6 +263,31 @@ plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_ou
 }
 plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
   return after(1, d_total, d_out, stream);
+}
+
+plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_result* d_out, void* d_ws,
+                         size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  if (stages < 0 || stages > kDpiMaxStages) return fail(PLUGIN_E_INVALID, "stages must be 0..5%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  plugin_result* s1 = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
+  if ((st = run_step1(d_x, n, s1, w, s)) != PLUGIN_OK) return st;
+  cudaError_t e;
+  if ((e = launch_dpi_init(s1, stages, d_out, s)) != cudaSuccess) return cuda_fail(e, "dpi init");
+  const int64_t tiles = psi_tiles(n);
+  for (int j = stages; j >= 1; --j) {
+    const int slot = j & 1;
+    if ((e = launch_psi(w.xs, n, 2 * j + 2, 0, 0.0, &d_out->g[j - 1], &d_out->status, w.ctrl, slot, 0, tiles, s)) !=
+        cudaSuccess)
+      return cuda_fail(e, "dpi pass");
+    if ((e = launch_dpi_finalize(w.ctrl, slot, j, d_out, s)) != cudaSuccess) return cuda_fail(e, "dpi finalize");
+  }
+  return PLUGIN_OK;
 }
 
 size_t kde_workspace_bytes(int64_t n, int64_t m) {

@@ -71,11 +71,14 @@ cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials
                          cudaStream_t s);
 cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
                         int64_t nblocks, cudaStream_t s);
-// mode: 0 = plugin pass r=6 (g from out->g1), 1 = plugin pass r=4 (g from out->g2),
-//       2 = psi_r with host g; | kPsiSkipUnderflow: skip tiles whose terms are all exactly 0
-constexpr int kPsiSkipUnderflow = 4;
-cudaError_t launch_psi(const float* xs, int64_t n, int r, int mode, double g_host, const plugin_result* out,
-                       Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, cudaStream_t s);
+// One pass of Steps IV/VI (or Psi_r for any even r <= 12) over tiles [tile_begin, tile_end):
+// g from *g_dev (a device bandwidth; the pass is skipped unless *status_dev == PLUGIN_OK) or,
+// if g_dev is null, g_host.  skip != 0: skip tiles whose terms are all exactly 0 (NEXT 4).
+cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_host, const double* g_dev,
+                       const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end,
+                       cudaStream_t s);
+// |u| beyond which every fp32 term of a pass is exactly zero (psi.cu, fused.cu)
+constexpr double kSkipU = 13.25;
 // what: 0 = plugin r=6 finalize, 1 = plugin r=4 finalize, 2 = psi_r -> d_psi, 3 = export limbs
 cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* total, plugin_result* out,
                             int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
@@ -85,6 +88,10 @@ cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
 // 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
 constexpr int kFusedMaxGrid = 1024;
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s);
+// the l-stage direct plug-in (dpi.cu)
+constexpr int kDpiMaxStages = PLUGIN_DPI_MAX_STAGES;
+cudaError_t launch_dpi_init(const plugin_result* s1, int stages, plugin_dpi_result* out, cudaStream_t s);
+cudaError_t launch_dpi_finalize(Ctrl* ctrl, int slot, int j, plugin_dpi_result* out, cudaStream_t s);
 // KDE of Eq. 1-2 at m points over the sorted sample xs (kde.cu); `extra` holds
 // kde_extra_bytes(n, m) bytes of workspace
 size_t kde_extra_bytes(int64_t n, int64_t m);

@@ -102,7 +102,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
         tile_coords(t, nb, bi, bj);
         const int64_t i0 = bi * T, j0 = bj * T;
         if (skip && bi != bj &&
-            ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > 13.25)
+            ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
           continue;  // all terms exactly zero (psi.cu); uniform across the CTA
         const int jcount = (int)((n - j0) < T ? (n - j0) : T);
         const double w = (bi == bj) ? 1.0 : 2.0;

@@ -36,20 +36,19 @@ struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : 3; };
 
 template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
-psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, const plugin_result* __restrict__ out,
-           Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
+psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
+           const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
   constexpr int T = kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
 
-  // mode bit 2: skip tiles whose every term is exactly zero in fp32
-  const bool skip = (mode & kPsiSkipUnderflow) != 0;
-  mode &= 3;
+  // g: from the device (a bandwidth an earlier kernel of the stream computed; the pass is
+  // skipped if that chain already failed) or from the host
   double g = g_host;
-  if (mode == 0 || mode == 1) {
-    if (out->status != PLUGIN_OK) return;
-    g = (mode == 0) ? out->g1 : out->g2;
+  if (g_dev) {
+    if (*status_dev != PLUGIN_OK) return;
+    g = *g_dev;
   }
   const float s = __double2float_rn(1.0 / g);
   const int64_t nb = (n + T - 1) / T;
@@ -71,7 +70,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int mode, double g_host, con
       // rounding), every exponent a = t c + p_i is below -127 and ex2.approx.ftz returns +0
       // exactly, so the tile adds exactly nothing (bit-identical to evaluating it)
       const double gap = (double)__ldg(xs + j0) - (double)__ldg(xs + i0 + T - 1);
-      if (gap * (double)s * (1.0 - 1e-5) > 13.25) {
+      if (gap * (double)s * (1.0 - 1e-5) > kSkipU) {
         __syncthreads();  // every thread has read s_tile before thread 0 overwrites it
         continue;
       }
@@ -115,8 +114,8 @@ int psi_rows_per_thread(int64_t n) {
 }
 
 template <int R, int ORDER>
-static cudaError_t launch_t(const float* xs, int64_t n, int mode, double g, const plugin_result* out, Ctrl* ctrl,
-                            int slot, int64_t tb, int64_t te, cudaStream_t s) {
+static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, const double* g_dev,
+                            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tb, int64_t te, cudaStream_t s) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 0, occ = 0;
@@ -128,24 +127,28 @@ static cudaError_t launch_t(const float* xs, int64_t n, int mode, double g, cons
   int64_t tiles = te - tb;
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;
-  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, mode, g, out, ctrl, slot, tb, te);
+  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te);
   return cudaGetLastError();
 }
 
-cudaError_t launch_psi(const float* xs, int64_t n, int r, int mode, double g_host, const plugin_result* out,
-                       Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, cudaStream_t s) {
+cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_host, const double* g_dev,
+                       const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end,
+                       cudaStream_t s) {
   const int R = psi_rows_per_thread(n);
   if (tile_end <= tile_begin) return cudaSuccess;
-#define PLG_CASE(RR)                                                                              \
-  if (R == RR) {                                                                                  \
-    return r == 6 ? launch_t<RR, 6>(xs, n, mode, g_host, out, ctrl, slot, tile_begin, tile_end, s) \
-                  : launch_t<RR, 4>(xs, n, mode, g_host, out, ctrl, slot, tile_begin, tile_end, s); \
+#define PLG_ORDER(RR, OO)                                                                                  \
+  if (r == OO) return launch_t<RR, OO>(xs, n, skip, g_host, g_dev, status_dev, ctrl, slot, tile_begin, tile_end, s);
+#define PLG_CASE(RR)                                                                                       \
+  if (R == RR) {                                                                                           \
+    PLG_ORDER(RR, 6) PLG_ORDER(RR, 4) PLG_ORDER(RR, 0) PLG_ORDER(RR, 2) PLG_ORDER(RR, 8) PLG_ORDER(RR, 10) \
+    PLG_ORDER(RR, 12)                                                                                      \
   }
   PLG_CASE(8)
   PLG_CASE(4)
   PLG_CASE(2)
   PLG_CASE(1)
 #undef PLG_CASE
+#undef PLG_ORDER
   return cudaErrorInvalidValue;
 }
 

@@ -33,6 +33,43 @@ __device__ __forceinline__ int row_scale_offset(int64_t i) {
   return (int)(((h >> 16) * 15u) >> 16) - 7;
 }
 
+// He_r(u) for even r as a polynomial in t = u^2 by Horner, monic, exact integer coefficients
+// (probabilists' Hermite; K^(r)(u) = He_r(u) phi(u), r = 4, 6: the printed polynomials of
+// Steps VI/IV).  All coefficients are exact in fp32 (< 2^24).
+template <int ORDER>
+__device__ __forceinline__ u64 hermite_t(u64 t) {
+  u64 p;
+  if (ORDER == 2) {
+    p = add2(t, 0xBF800000BF800000ull);      // t - 1
+  } else if (ORDER == 4) {
+    p = add2(t, 0xC0C00000C0C00000ull);      // t - 6
+    p = fma2(p, t, 0x4040000040400000ull);   // (t - 6) t + 3
+  } else if (ORDER == 6) {
+    p = add2(t, 0xC1700000C1700000ull);      // t - 15
+    p = fma2(p, t, 0x4234000042340000ull);   // (t - 15) t + 45
+    p = fma2(p, t, 0xC1700000C1700000ull);   // ((t - 15) t + 45) t - 15
+  } else if (ORDER == 8) {
+    p = add2(t, 0xC1E00000C1E00000ull);      // t - 28
+    p = fma2(p, t, 0x4352000043520000ull);   // + 210
+    p = fma2(p, t, 0xC3D20000C3D20000ull);   // - 420
+    p = fma2(p, t, 0x42D2000042D20000ull);   // + 105
+  } else if (ORDER == 10) {
+    p = add2(t, 0xC2340000C2340000ull);      // t - 45
+    p = fma2(p, t, 0x441D8000441D8000ull);   // + 630
+    p = fma2(p, t, 0xC544E000C544E000ull);   // - 3150
+    p = fma2(p, t, 0x4593A8004593A800ull);   // + 4725
+    p = fma2(p, t, 0xC46C4000C46C4000ull);   // - 945
+  } else {  // ORDER == 12
+    p = add2(t, 0xC2840000C2840000ull);      // t - 66
+    p = fma2(p, t, 0x44B9A00044B9A000ull);   // + 1485
+    p = fma2(p, t, 0xC6589000C6589000ull);   // - 13860
+    p = fma2(p, t, 0x474B0700474B0700ull);   // + 51975
+    p = fma2(p, t, 0xC773A200C773A200ull);   // - 62370
+    p = fma2(p, t, 0x46226C0046226C00ull);   // + 10395
+  }
+  return p;
+}
+
 template <int ORDER, bool MASK>
 __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, bool m0 = true, bool m1 = true) {
   const u64 c2 = 0xBF38AA3BBF38AA3Bull;  // {fp32(-log2(e)/2)} x 2 = -0.72134752f
@@ -48,16 +85,11 @@ __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, 
     e1 = m1 ? e1 : 0.f;
   }
   u64 e = pk2(e0, e1);
-  u64 p;
-  if (ORDER == 6) {
-    p = add2(t, 0xC1700000C1700000ull);      // t - 15
-    p = fma2(p, t, 0x4234000042340000ull);   // (t - 15) t + 45
-    p = fma2(p, t, 0xC1700000C1700000ull);   // ((t - 15) t + 45) t - 15
-  } else {
-    p = add2(t, 0xC0C00000C0C00000ull);      // t - 6
-    p = fma2(p, t, 0x4040000040400000ull);   // (t - 6) t + 3
+  if (ORDER == 0) {  // K = phi: P = He_0 = 1
+    acc = add2(acc, e);
+    return;
   }
-  acc = fma2(p, e, acc);
+  acc = fma2(hermite_t<ORDER>(t), e, acc);
 }
 
 __device__ __forceinline__ Fx128 fx_from_double(double x) {

@@ -35,6 +35,23 @@ class plugin_result(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
+DPI_MAX_STAGES = 5
+
+
+class plugin_dpi_result(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("stages", ctypes.c_int32), ("n", ctypes.c_int64),
+                ("mean", ctypes.c_double), ("var", ctypes.c_double), ("sigma", ctypes.c_double),
+                ("psi_ns_z", ctypes.c_double)] + [
+        (k, ctypes.c_double * DPI_MAX_STAGES) for k in ("g_z", "g", "psi_z", "psi")] + [
+        ("h_z", ctypes.c_double), ("h", ctypes.c_double)]
+
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        for k in ("g_z", "g", "psi_z", "psi"):   # stage j -> value (j = 1..stages)
+            d[k] = {j: d[k][j - 1] for j in range(1, self.stages + 1)}
+        return d
+
+
 class plugin_fx128(ctypes.Structure):
     _fields_ = [("limb", ctypes.c_int64 * 4)]
 
@@ -65,6 +82,7 @@ def lib():
             "plugin_after_psi4": (i32, [P, P, P]),
             "plugin_num_tiles": (i64, [i64]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
             "kde_workspace_bytes": (sz, [i64, i64]),
             "kde_eval": (i32, [P, i64, d, P, i64, P, P, sz, P]),
             "plugin_last_error": (ctypes.c_char_p, []),
@@ -83,7 +101,7 @@ PLUGIN_MULTI_KERNEL = 2
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
+            "plugin_shard_tiles", "plugin_dpi", "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
 
 
 def _check(st: int):
@@ -213,6 +231,25 @@ def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
     lib().plugin_shard_tiles(n, rank, world, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+DPI_RESULT_BYTES = ctypes.sizeof(plugin_dpi_result)
+
+
+def plugin_dpi(x: torch.Tensor, stages: int, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """l-stage direct plug-in (Alg. 1 is stages = 2) on the device; returns the result buffer."""
+    x = _x(x)
+    n = x.numel()
+    ws = workspace(n, x.device) if ws is None else ws
+    out = torch.empty(DPI_RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
+    _check(lib().plugin_dpi(x.data_ptr(), n, int(stages), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                            _stream(stream)))
+    return out
+
+
+def read_dpi_result(buf: torch.Tensor) -> dict:
+    return plugin_dpi_result.from_buffer_copy(buf.detach().to("cpu").numpy().tobytes()).to_dict()
 
 
 def kde_workspace_bytes(n: int, m: int) -> int:
