@@ -430,7 +430,11 @@ def run_kde(a):
     visited = kde_terms_visited(xh, h, pts)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
-    peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
+    mufu_only = os.environ.get("PLUGIN_KDE_MUFU_ONLY") == "1"
+    # MUFU-only: 16 ex2/clk/SM.  Hybrid (default): 3 of 4 terms on MUFU (4 FP32 lane-ops each),
+    # 1 of 4 with a 12-lane-op FMA-pipe exp2: min(16 / (3/4), 128 / (4 + 8/4)) = 21.33 terms/clk/SM
+    per_clk = MUFU_EX2_PER_CLK_PER_SM if mufu_only else 64.0 / 3.0
+    peak = per_clk * sms * f_meas * 1e6 / 1e9
     achieved = visited / (ms / 1e3) / 1e9
     # end to end from host memory: H2D of X and the points, D2H of the curve
     xpin, ppin = torch.from_numpy(xh).pin_memory(), torch.from_numpy(pts).pin_memory()
@@ -454,8 +458,11 @@ def run_kde(a):
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GTerms/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "kde_kernel",
-                         "peak_basis": f"{MUFU_EX2_PER_CLK_PER_SM} MUFU.EX2/clk/SM x {sms} SMs x {f_meas:.0f} MHz "
-                                       "(1 ex2 per visited term)"},
+                         "peak_basis": (f"{per_clk:.2f} terms/clk/SM x {sms} SMs x {f_meas:.0f} MHz ("
+                                        + ("MUFU.EX2-bound, 1 ex2 per visited term" if mufu_only else
+                                           "MUFU + FMA pipes saturated together: 3/4 of the exps on MUFU.EX2, "
+                                           "1/4 on the FMA pipe") + ")"),
+                         "variant": "mufu_only" if mufu_only else "hybrid"},
             "e2e": {"value": n * m / statistics.median(ts) / 1e9, "unit": "GTerms/s",
                     "h2d_bytes_per_step": 4 * (n + m), "d2h_bytes_per_step": 8 * m,
                     "seconds_per_step": statistics.median(ts)},

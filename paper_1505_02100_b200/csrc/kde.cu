@@ -11,11 +11,15 @@
 // [lower_bound(min - C), upper_bound(max + C)).  That range is split into S equal segments,
 // one CTA per (block, segment), so small point sets still fill the 148 SMs.  Per term:
 //     d = x_k - X_i (fp32)   a = (d * k) * d   e = ex2.approx(a)   acc += e
-// two terms per packed f32x2 instruction: 4 FP32 lane-ops + 1 MUFU.EX2 per term.  fp32
+// two terms per packed f32x2 instruction: 4 FP32 lane-ops + 1 MUFU.EX2 per term.  MUFU.EX2
+// (16/clk/SM) would bind at 16 terms/clk/SM with the FMA pipe half idle, so one term in four
+// evaluates its exp2 on the FMA pipe instead (kde_term2_poly: 8 more FP32 lane-ops): both
+// pipes then saturate together at 21.3 terms/clk/SM.  fp32
 // accumulators hold 64 terms per point, then go to per-point fp64; each CTA writes its fp64
 // per-point partials and the last CTA of a block adds the S partials in segment order
 // (deterministic) and scales by phi(0) / (n h).
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "simd.cuh"
@@ -45,6 +49,32 @@ __device__ __forceinline__ void kde_term2_masked(u64 xj, u64 p, u64 k2, u64& acc
   acc = add2(acc, pk2(e0, e1));
 }
 
+// exp2 on the FMA pipe for the hybrid variant: a = n + f, n = rint(a) (magic-number add),
+// f in [-1/2, 1/2], 2^f by a degree-5 minimax polynomial (relative error 7.5e-8; 2.3e-7 with
+// fp32 evaluation), 2^n by adding n to the exponent field.  a is clamped at -126 (the result
+// stays a normal float; MUFU.EX2 would flush such terms to 0: the difference is < 2^-125.5
+// per term).
+__device__ __forceinline__ void kde_term2_poly(u64 xj, u64 p, u64 k2, u64& acc) {
+  const u64 kMagic = 0x4B4000004B400000ull;  // 1.5 * 2^23
+  const u64 d = sub2(p, xj);
+  float a0, a1;
+  upk2(mul2(mul2(d, k2), d), a0, a1);
+  const u64 a = pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f));
+  const u64 r = add2(a, kMagic);           // rint(a) in the low mantissa bits
+  const u64 f = sub2(a, sub2(r, kMagic));  // a - rint(a), exact
+  u64 q = fma2(0x3AAE04733AAE0473ull, f, 0x3C1E86293C1E8629ull);  // c5 f + c4
+  q = fma2(q, f, 0x3D635B723D635B72ull);   // + c3
+  q = fma2(q, f, 0x3E75FC8C3E75FC8Cull);   // + c2
+  q = fma2(q, f, 0x3F3172143F317214ull);   // + c1
+  q = fma2(q, f, 0x3F8000013F800001ull);   // + c0
+  float r0, r1, q0, q1;
+  upk2(r, r0, r1);
+  upk2(q, q0, q1);
+  const float e0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(r0) << 23));
+  const float e1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(r1) << 23));
+  acc = add2(acc, pk2(e0, e1));
+}
+
 // first index i in [0, n) with xs[i] >= v (strict = false) or xs[i] > v (strict = true)
 __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
   int64_t lo = 0, hi = n;
@@ -57,6 +87,7 @@ __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
   return lo;
 }
 
+template <bool HYB>
 __global__ void __launch_bounds__(kKdeThreads, 2)
 kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pts, int64_t m, float kf, double cut,
            int S, double scale, const Ctrl* ctrl, double* __restrict__ partial, unsigned int* __restrict__ counters,
@@ -121,7 +152,9 @@ kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pt
 #pragma unroll
         for (int k = 0; k < kKdeRG; ++k) {
           kde_term2(j01, p2[k], k2, acc[k]);
-          kde_term2(j23, p2[k], k2, acc[k]);
+          // hybrid: one term pair in four takes its exp on the FMA pipe (kHybFrac = 1/4)
+          if (HYB && (q & 1)) kde_term2_poly(j23, p2[k], k2, acc[k]);
+          else kde_term2(j23, p2[k], k2, acc[k]);
         }
       }
 #pragma unroll
@@ -184,6 +217,16 @@ kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pt
   }
 }
 
+// hybrid MUFU / FMA-pipe exp (default); PLUGIN_KDE_MUFU_ONLY=1 selects the MUFU-only kernel
+bool kde_hybrid() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PLUGIN_KDE_MUFU_ONLY");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int64_t kde_point_blocks(int64_t m) { return (m + kKdeGB - 1) / kKdeGB; }
 
 int kde_segments(int64_t n, int64_t m) {
@@ -218,8 +261,12 @@ cudaError_t launch_kde(const float* xs, int64_t n, double h, const float* pts, i
   const float kf = (float)kd;
   const double cut = sqrt(126.5 / fabs((double)kf)) * (1.0 + 1e-6);
   const double scale = kInvSqrt2Pi / ((double)n * h);
-  kde_kernel<<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, cut, S, scale, ctrl, partial,
-                                                              counters, f);
+  if (kde_hybrid())
+    kde_kernel<true><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, cut, S, scale, ctrl, partial,
+                                                                    counters, f);
+  else
+    kde_kernel<false><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, cut, S, scale, ctrl,
+                                                                     partial, counters, f);
   return cudaGetLastError();
 }
 
