@@ -84,6 +84,14 @@ def lib():
         L.oracle_psi_literal_sum.argtypes = [P, i64, d, i32]
         L.oracle_kde.restype = None
         L.oracle_kde.argtypes = [P, i64, d, P, i64, i32, P]
+        L.oracle_q32_mul.restype = i64
+        L.oracle_q32_mul.argtypes = [i64, i64]
+        L.oracle_q32_exp.restype = i64
+        L.oracle_q32_exp.argtypes = [i64]
+        L.oracle_q32_term.restype = i64
+        L.oracle_q32_term.argtypes = [i64, i64, i32]
+        L.oracle_q32_psi_sum.restype = None
+        L.oracle_q32_psi_sum.argtypes = [P, i64, i64, i32, i32, P]
         L.oracle_max_threads.restype = i32
         L.oracle_max_threads.argtypes = []
         _lib = L
@@ -317,6 +325,68 @@ def dpi(x, stages: int, threads: int = 0) -> dict:
     res["h_z"] = h_z
     res["h"] = h_z * sigma
     return res
+
+
+# ---- the paper's Q32.32 fixed-point datapath ---------
+Q32_ONE = 1 << 32
+
+
+def q32_encode(v) -> np.ndarray:
+    """Q2: real -> Q32.32 raw int64, round to nearest, ties away from zero."""
+    v = np.asarray(v, dtype=np.float64)
+    s = v * float(Q32_ONE)                       # exact (power-of-two scaling)
+    return (np.sign(s) * np.floor(np.abs(s) + 0.5)).astype(np.int64)
+
+
+def q32_mul(a: int, b: int) -> int:
+    return lib().oracle_q32_mul(int(a), int(b))
+
+
+def q32_exp(x: int) -> int:
+    return lib().oracle_q32_exp(int(x))
+
+
+def q32_term(d: int, rg: int, r: int) -> int:
+    return lib().oracle_q32_term(int(d), int(rg), int(r))
+
+
+def q32_psi_sum(zq, rg: int, r: int, threads: int = 0) -> int:
+    """sum_{i<j} term(z_i - z_j) in Q32.32 raw units, as an exact Python int (int128)."""
+    zq = np.ascontiguousarray(zq, dtype=np.int64)
+    out = np.zeros(2, dtype=np.int64)
+    lib().oracle_q32_psi_sum(_ptr(zq), zq.size, int(rg), int(r), int(threads), _ptr(out))
+    return int(out[1]) * (1 << 64) + (int(out[0]) & ((1 << 64) - 1))
+
+
+def q32_psi(zq, g: float, r: int, threads: int = 0) -> dict:
+    """Psi_r(g) of Steps IV/VI with the pair sum in Q32.32 (z units): rg = encode(1/g) (the
+    hoisted reciprocal of Fig. 5), S = 2 sum_{i<j} term + n term(0), then
+    Psi = phi(0) (S / 2^32) / (n^2 g^(r+1)) in fp64."""
+    zq = np.ascontiguousarray(zq, dtype=np.int64)
+    n = zq.size
+    rg = int(q32_encode(1.0 / g))
+    half = q32_psi_sum(zq, rg, r, threads)
+    total = 2 * half + n * q32_term(0, rg, r)
+    return {"rg": rg, "half_sum": half, "total": total,
+            "psi": (total / float(Q32_ONE)) / math.sqrt(2.0 * PI) / (n * n * g ** (r + 1))}
+
+
+def q32_plugin(x, threads: int = 0) -> dict:
+    """Alg. 1 with the Steps IV/VI pair sums in Q32.32 (the paper's datapath, "fast" loop of
+    Fig. 5) on the z-scored sample (Eq. 3, encoded to Q32.32); the O(1) steps in fp64."""
+    x = _f32(x)
+    n = int(x.size)
+    s1 = step1(x)
+    sigma = s1["sigma"]
+    zq = q32_encode(zscore(x, s1["mean"], sigma))
+    g1_z = g1_bandwidth(psi8_ns(1.0), n)
+    p6 = q32_psi(zq, g1_z, 6, threads)
+    g2_z = g2_bandwidth(p6["psi"], n)
+    p4 = q32_psi(zq, g2_z, 4, threads)
+    h_z = h_bandwidth(p4["psi"], n)
+    return {"n": n, "sigma": sigma, "g1_z": g1_z, "psi6_z": p6["psi"], "g2_z": g2_z, "psi4_z": p4["psi"],
+            "h_z": h_z, "h": h_z * sigma, "S6_q32": p6["total"], "S4_q32": p4["total"],
+            "rg1": p6["rg"], "rg2": p4["rg"]}
 
 
 # ---- Eq. 1-2: the kernel density estimate that h is for (SURVEY §8(f) NEXT 1) ----------

@@ -220,6 +220,100 @@ void oracle_kde(const float* X, int64_t n, double h, const double* xk, int64_t m
   }
 }
 
+/* ======================================================================================
+ * The paper's Q32.32 fixed-point datapath for Steps IV/VI (Fig. 5 "fast" loop;
+ * SURVEY §8(f) NEXT 2), written from its definition in DESIGN.md §14 (readings Q1-Q7).
+ * A Q32.32 number is an int64 raw value v, meaning v / 2^32.  Integer arithmetic only: the
+ * result is exact and independent of summation order.
+ * ====================================================================================== */
+typedef __int128 i128;
+
+/* Q1: multiplication = the 128-bit product shifted right by 32 (floor, i.e. truncation toward
+ * -inf, the SPEC ledger's choice; P:208-213 fix Q32.32 but not the rounding) */
+int64_t oracle_q32_mul(int64_t a, int64_t b) { return (int64_t)(((i128)a * (i128)b) >> 32); }
+static int64_t q62_mul(int64_t a, int64_t b) { return (int64_t)(((i128)a * (i128)b) >> 62); }
+
+/* Q3: e^x for x <= 0 (the only arguments Steps IV/VI need): x = k ln2 + w, k = round(x/ln2),
+ * e^w by its Taylor polynomial of degree 9 in Q2.62 (coefficients round(2^62/i!)), then a
+ * right shift by -k.  e^x = 0 below x = -21 (SPEC ledger underflow clamp). */
+static const int64_t Q32_LN2 = 2977044472LL;         /* round(ln 2 * 2^32)  */
+static const int64_t Q32_INV_LN2 = 6196328019LL;     /* round(2^32 / ln 2)  */
+
+/* c_i = round(2^62 / i!), i = 0..9 (exact integer arithmetic, ties up) */
+static void q32_taylor(int64_t* c) {
+  i128 fact = 1;
+  for (int i = 0; i < 10; ++i) {
+    if (i > 0) fact *= i;
+    const i128 num = ((i128)1) << 62;
+    c[i] = (int64_t)((num + fact / 2) / fact);
+  }
+}
+
+static int64_t q32_exp_c(const int64_t* c, int64_t x) {
+  if (x < -21LL * 4294967296LL) return 0;
+  const int64_t y = oracle_q32_mul(x, Q32_INV_LN2);
+  const int64_t k = (y + 2147483648LL) >> 32;        /* round half up */
+  const int64_t w = x - k * Q32_LN2;
+  const int64_t w62 = w * 1073741824LL;               /* Q32.32 -> Q2.62 */
+  int64_t p = c[9];
+  for (int i = 8; i >= 0; --i) p = q62_mul(p, w62) + c[i];
+  const int64_t sh = 30 - k;
+  return sh >= 63 ? 0 : (p >> sh);
+}
+
+int64_t oracle_q32_exp(int64_t x) {
+  int64_t c[10];
+  q32_taylor(c);
+  return q32_exp_c(c, x);
+}
+
+/* Q4-Q5: the pair term of Steps IV/VI in Q32.32, K^(r)(u)/phi(0) with u = |d| * rg:
+ * t = u^2; 0 if t > 42 (e^{-t/2} = 0 below -21); else P_r(t) * e^{-t/2} with the printed
+ * polynomials evaluated by Horner in Q32.32. */
+static int64_t q32_term_c(const int64_t* c, int64_t d, int64_t rg, int r) {
+  const int64_t one = 4294967296LL;
+  const int64_t a = d < 0 ? -d : d;
+  const int64_t u = oracle_q32_mul(a, rg);
+  const int64_t t = oracle_q32_mul(u, u);
+  if (t > 42 * one) return 0;
+  const int64_t e = q32_exp_c(c, -(t >> 1));
+  int64_t P;
+  if (r == 4) P = oracle_q32_mul(t, t) - 6 * t + 3 * one;
+  else P = oracle_q32_mul(oracle_q32_mul(t - 15 * one, t) + 45 * one, t) - 15 * one;
+  return oracle_q32_mul(P, e);
+}
+
+int64_t oracle_q32_term(int64_t d, int64_t rg, int r) {
+  int64_t c[10];
+  q32_taylor(c);
+  return q32_term_c(c, d, rg, r);
+}
+
+/* The halved sum of Eq. 6/7 in Q32.32: out = sum_{i<j} term(z_i - z_j) as an exact int128
+ * (out[0] = low 64 bits, out[1] = high 64 bits, two's complement).  Rows in parallel, each
+ * an exact integer sum: identical for any thread count and any order. */
+void oracle_q32_psi_sum(const int64_t* zq, int64_t n, int64_t rg, int r, int nthreads, int64_t* out) {
+  i128 total = 0;
+  int64_t c[10];
+  q32_taylor(c);
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  i128* row = (i128*)malloc(sizeof(i128) * (size_t)(n > 0 ? n : 1));
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t i = 0; i < n; ++i) {
+    i128 acc = 0;
+    for (int64_t j = i + 1; j < n; ++j) acc += q32_term_c(c, zq[i] - zq[j], rg, r);
+    row[i] = acc;
+  }
+  for (int64_t i = 0; i < n; ++i) total += row[i];
+  free(row);
+  out[0] = (int64_t)(uint64_t)total;
+  out[1] = (int64_t)(total >> 64);
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
