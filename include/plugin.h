@@ -180,6 +180,30 @@ typedef struct {
 plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_result* d_out,
                          void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---- the paper's own Q32.32 fixed-point datapath ---- */
+
+/*
+ * The FPGA design computes in Q32.32 fixed point with a hoisted reciprocal and a
+ * polynomial exp in the hot loop (Fig. 5 "fast").  Here the pair sums of Steps IV/VI
+ * run in that arithmetic on the integer pipes (definitions Q1-Q7 of DESIGN.md §14: floor-
+ * truncating 128-bit multiplies, a Q2.62 Taylor exp with the e^-21 clamp, the symmetric pair
+ * term of |z_i - z_j|); sums are exact 128-bit integers, so results are order-free and equal the
+ * oracle's bit for bit.  A Q32.32 value is an int64 raw r meaning r / 2^32.
+ *
+ * psi_r_q32: *d_total (device int64[2], low then high 64 bits of a two's-complement int128) =
+ *   sum_i sum_j term(zq_i - zq_j) over ALL ordered pairs (Eq. 5-7's left side), r in {4, 6};
+ *   d_zq device int64[n] (Q32.32, |z| < 2^20), rg_q = Q32.32 reciprocal bandwidth in (0, 2^52).
+ *   Psi_r(g) = phi(0) (total / 2^32) / (n^2 g^(r+1)).  Needs plugin_workspace_bytes(n).
+ * plugin_h_q32: Algorithm 1 with both pair passes in Q32.32 on the z-scored sample (Eq. 3,
+ *   encoded on the device) and the O(1) steps in fp64 (as plugin_h); needs
+ *   plugin_q32_workspace_bytes(n).  Its h agrees with the fp64 h to the paper's Table 4 bound.
+ */
+size_t plugin_q32_workspace_bytes(int64_t n);
+plugin_status psi_r_q32(const int64_t* d_zq, int64_t n, int64_t rg_q, int r, int64_t* d_total,
+                        void* d_ws, size_t ws_bytes, void* stream);
+plugin_status plugin_h_q32(const float* d_x, int64_t n, plugin_result* d_out,
+                           void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- the estimate the bandwidth is for ---- */
 
 /* Bytes of workspace kde_eval needs for n samples and m points (>= plugin_workspace_bytes(n)). */

@@ -290,6 +290,56 @@ plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_res
   return PLUGIN_OK;
 }
 
+size_t plugin_q32_workspace_bytes(int64_t n) {
+  if (n < 1) n = 1;
+  return layout(n).total + align_up(sizeof(long long) * (size_t)n, 256) + 256;
+}
+
+plugin_status psi_r_q32(const int64_t* d_zq, int64_t n, int64_t rg_q, int r, int64_t* d_total, void* d_ws,
+                        size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_zq || !d_total) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  if (r != 4 && r != 6) return fail(PLUGIN_E_INVALID, "r must be 4 or 6%s (r=%lld)", "", r);
+  if (rg_q <= 0 || rg_q >= ((int64_t)1 << 52)) return fail(PLUGIN_E_INVALID, "rg_q must be in (0, 2^52)%s");
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
+  if ((e = launch_psi_q32(reinterpret_cast<const long long*>(d_zq), n, rg_q, nullptr, nullptr, r, w.ctrl, 1,
+                          reinterpret_cast<long long*>(d_total), -1, nullptr, nullptr, s)) != cudaSuccess)
+    return cuda_fail(e, "psi q32");
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_h_q32(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes,
+                           void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 2);
+  if (st != PLUGIN_OK) return st;
+  if (ws_bytes < plugin_q32_workspace_bytes(n))
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)plugin_q32_workspace_bytes(n));
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  char* b = static_cast<char*>(d_ws);
+  long long* zq = reinterpret_cast<long long*>(b + w.L.total);
+  long long* rg = reinterpret_cast<long long*>(b + w.L.total + align_up(sizeof(long long) * (size_t)n, 256));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
+  cudaError_t e;
+  if ((e = launch_q32_encode(w.xs, n, d_out, zq, s)) != cudaSuccess) return cuda_fail(e, "q32 encode");
+  if ((e = launch_q32_rg1(d_out, rg, s)) != cudaSuccess) return cuda_fail(e, "q32 rg1");
+  if ((e = launch_psi_q32(zq, n, 0, rg, &d_out->status, 6, w.ctrl, 0, nullptr, 0, d_out, rg + 1, s)) != cudaSuccess)
+    return cuda_fail(e, "q32 psi6");
+  if ((e = launch_psi_q32(zq, n, 0, rg + 1, &d_out->status, 4, w.ctrl, 1, nullptr, 1, d_out, nullptr, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "q32 psi4");
+  return PLUGIN_OK;
+}
+
 size_t kde_workspace_bytes(int64_t n, int64_t m) {
   if (n < 1) n = 1;
   if (m < 0) m = 0;

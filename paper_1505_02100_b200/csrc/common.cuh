@@ -88,6 +88,14 @@ cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
 // 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
 constexpr int kFusedMaxGrid = 1024;
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s);
+// the Q32.32 datapath (q32.cu): one pass over the Q32.32 sample zq with rg from rg_dev (or
+// rg_host), its exact 128-bit total to out[2] (if out) and, with res, the PLUGIN finalize of
+// pass `what` (rg_next <- encode(1/g2_z) after pass 0)
+cudaError_t launch_psi_q32(const long long* zq, int64_t n, long long rg_host, const long long* rg_dev,
+                           const int32_t* status_dev, int r, Ctrl* ctrl, int slot, long long* out, int what,
+                           plugin_result* res, long long* rg_next, cudaStream_t s);
+cudaError_t launch_q32_encode(const float* xs, int64_t n, const plugin_result* s1, long long* zq, cudaStream_t s);
+cudaError_t launch_q32_rg1(const plugin_result* res, long long* rg, cudaStream_t s);
 // the l-stage direct plug-in (dpi.cu)
 constexpr int kDpiMaxStages = PLUGIN_DPI_MAX_STAGES;
 cudaError_t launch_dpi_init(const plugin_result* s1, int stages, plugin_dpi_result* out, cudaStream_t s);

@@ -83,6 +83,9 @@ def lib():
             "plugin_num_tiles": (i64, [i64]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
+            "plugin_q32_workspace_bytes": (sz, [i64]),
+            "psi_r_q32": (i32, [P, i64, i64, i32, P, P, sz, P]),
+            "plugin_h_q32": (i32, [P, i64, P, P, sz, P]),
             "kde_workspace_bytes": (sz, [i64, i64]),
             "kde_eval": (i32, [P, i64, d, P, i64, P, P, sz, P]),
             "plugin_last_error": (ctypes.c_char_p, []),
@@ -101,7 +104,8 @@ PLUGIN_MULTI_KERNEL = 2
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_dpi", "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
+            "plugin_shard_tiles", "plugin_dpi", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
+            "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
 
 
 def _check(st: int):
@@ -250,6 +254,34 @@ def plugin_dpi(x: torch.Tensor, stages: int, out: torch.Tensor | None = None, ws
 
 def read_dpi_result(buf: torch.Tensor) -> dict:
     return plugin_dpi_result.from_buffer_copy(buf.detach().to("cpu").numpy().tobytes()).to_dict()
+
+
+def psi_r_q32(zq: torch.Tensor, rg_q: int, r: int, ws: torch.Tensor | None = None, stream=None) -> int:
+    """sum_i sum_j term(zq_i - zq_j) in Q32.32 (NEXT 2) as an exact Python int (synchronises)."""
+    if not (isinstance(zq, torch.Tensor) and zq.is_cuda and zq.dtype == torch.int64 and zq.dim() == 1):
+        raise TypeError("zq must be a 1-D CUDA int64 tensor (Q32.32 raw values)")
+    zq = zq.contiguous()
+    n = zq.numel()
+    ws = workspace(n, zq.device) if ws is None else ws
+    out = torch.zeros(2, dtype=torch.int64, device=zq.device)
+    _check(lib().psi_r_q32(zq.data_ptr(), n, int(rg_q), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                           _stream(stream)))
+    lo, hi = out.cpu().tolist()
+    return hi * (1 << 64) + (lo & ((1 << 64) - 1))
+
+
+def plugin_h_q32(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """Alg. 1 with the Q32.32 pair passes (asynchronous); returns the device result buffer."""
+    x = _x(x)
+    n = x.numel()
+    if ws is None:
+        nbytes = lib().plugin_q32_workspace_bytes(n)
+        t = torch.empty(nbytes + 256, dtype=torch.uint8, device=x.device)
+        off = (-t.data_ptr()) % 256
+        ws = t[off:off + nbytes]
+    out = new_result(x.device) if out is None else out
+    _check(lib().plugin_h_q32(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
 
 
 def kde_workspace_bytes(n: int, m: int) -> int:
