@@ -43,8 +43,10 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--workload", default="plugin", choices=["plugin", "kde"],
-                    help="plugin: Alg. 1 (the headline); kde: Eq. 1-2 on a 65536-point curve (NEXT 1)")
+    ap.add_argument("--workload", default="plugin", choices=["plugin", "kde", "q32", "dpi"],
+                    help="plugin: Alg. 1 (the headline); kde: Eq. 1-2 on a 65536-point curve (NEXT 1); "
+                         "q32: Alg. 1 with the Q32.32 pair passes (NEXT 2); dpi: the l-stage plug-in (NEXT 3)")
+    ap.add_argument("--stages", type=int, default=3, help="dpi workload: l")
     ap.add_argument("--kde-points", type=int, default=65536)
     ap.add_argument("--skip-underflow", action="store_true",
                     help="plugin workload, 1 GPU: PLUGIN_SKIP_UNDERFLOW (bit-identical result; reports the "
@@ -471,12 +473,68 @@ def run_kde(a):
     return 0
 
 
+def run_variant(a):
+    """1 GPU, one step = plugin_h_q32 (q32) or plugin_dpi(l) (dpi) on config k; pair rate over the
+    unique pairs of all passes of the step."""
+    import torch
+
+    from paper_1505_02100_b200 import inputs
+    from paper_1505_02100_b200 import plugin as P
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    xh = inputs.config_data(a.config)
+    n = xh.size
+    x = torch.from_numpy(xh).to(dev)
+    if a.workload == "q32":
+        out = P.new_result(dev)
+        ws = torch.empty(P.lib().plugin_q32_workspace_bytes(n) + 256, dtype=torch.uint8, device=dev)
+        ws = ws[(-ws.data_ptr()) % 256:][:P.lib().plugin_q32_workspace_bytes(n)]
+        step = lambda: P.plugin_h_q32(x, out=out, ws=ws)  # noqa: E731
+        passes, launches = 2, 20
+    else:
+        out = torch.empty(P.DPI_RESULT_BYTES, dtype=torch.uint8, device=dev)
+        ws = P.workspace(n, dev)
+        step = lambda: P.plugin_dpi(x, a.stages, out=out, ws=ws)  # noqa: E731
+        passes, launches = a.stages, 15 + 2 * a.stages
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    for s in range(a.steps):
+        flush.fill_(s & 0xff)
+        ev[s][0].record(stream)
+        step()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in ev])
+    pairs = passes * n * (n - 1) // 2
+    res = P.read_result(out) if a.workload == "q32" else P.read_dpi_result(out)
+    what = ("Alg. 1 with both pair passes in Q32.32 fixed point (plugin_h_q32)" if a.workload == "q32"
+            else f"{a.stages}-stage direct plug-in (plugin_dpi), passes r = {2 * a.stages + 2}..4")
+    line = {"metric": f"pair evaluations/sec, {a.workload} variant", "value": pairs / (ms / 1e3) / 1e9,
+            "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "q32.32 (int64)" if a.workload == "q32" else "f32", "data": "synthetic",
+            "config": {"workload": f"cfg{a.config} n={n}: {what}", "pairs_per_step": pairs},
+            "h": res["h"], "status": res["status"], "clocks": clocks, "gpu_launches": launches * a.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     a = _args()
     if a.impl == "reference":
         return run_reference(a)
     if a.workload == "kde":
         return run_kde(a)
+    if a.workload in ("q32", "dpi"):
+        return run_variant(a)
     if a.skip_underflow:
         return run_skip(a)
     return run_ours(a)
