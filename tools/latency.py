@@ -46,6 +46,7 @@ def main():
     a = ap.parse_args()
     cases = [(f"paper n={n} N(0,1) seed {100 + k}", inputs.normal(n, 100 + k)) for k, n in
              enumerate(range(128, 1025, 128))]
+    cases += [(f"n={n} N(0,1) seed 7", inputs.normal(n, 7)) for n in (2048, 4096, 8192)]
     cases += [(f"cfg{k}", inputs.config_data(k)) for k in (1, 2, 3)]
     rows = []
     for name, xh in cases:
