@@ -55,24 +55,10 @@ __device__ __forceinline__ void kde_term2_masked(u64 xj, u64 p, u64 k2, u64& acc
 // stays a normal float; MUFU.EX2 would flush such terms to 0: the difference is < 2^-125.5
 // per term).
 __device__ __forceinline__ void kde_term2_poly(u64 xj, u64 p, u64 k2, u64& acc) {
-  const u64 kMagic = 0x4B4000004B400000ull;  // 1.5 * 2^23
   const u64 d = sub2(p, xj);
   float a0, a1;
   upk2(mul2(mul2(d, k2), d), a0, a1);
-  const u64 a = pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f));
-  const u64 r = add2(a, kMagic);           // rint(a) in the low mantissa bits
-  const u64 f = sub2(a, sub2(r, kMagic));  // a - rint(a), exact
-  u64 q = fma2(0x3AAE04733AAE0473ull, f, 0x3C1E86293C1E8629ull);  // c5 f + c4
-  q = fma2(q, f, 0x3D635B723D635B72ull);   // + c3
-  q = fma2(q, f, 0x3E75FC8C3E75FC8Cull);   // + c2
-  q = fma2(q, f, 0x3F3172143F317214ull);   // + c1
-  q = fma2(q, f, 0x3F8000013F800001ull);   // + c0
-  float r0, r1, q0, q1;
-  upk2(r, r0, r1);
-  upk2(q, q0, q1);
-  const float e0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(r0) << 23));
-  const float e1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(r1) << 23));
-  acc = add2(acc, pk2(e0, e1));
+  acc = add2(acc, ex2_fma2(pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f))));
 }
 
 // first index i in [0, n) with xs[i] >= v (strict = false) or xs[i] > v (strict = true)

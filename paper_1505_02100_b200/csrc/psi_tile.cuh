@@ -92,6 +92,35 @@ __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, 
   acc = fma2(hermite_t<ORDER>(t), e, acc);
 }
 
+// pair2 with the exp on the FMA pipe (ex2_fma2) instead of MUFU.EX2 (PSI_HYB4): results below
+// 2^-126 are set to +0 as MUFU.EX2.ftz flushes them, so all-zero tiles stay exactly zero.
+template <int ORDER>
+__device__ __forceinline__ void pair2_fma(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc) {
+  const u64 c2 = 0xBF38AA3BBF38AA3Bull;
+  u64 d = sub2(xj, xi);
+  u64 u = mul2(d, s2);
+  u64 t = mul2(u, u);
+  u64 a = fma2(t, c2, ph);
+  float a0, a1;
+  upk2(a, a0, a1);
+  float e0, e1;
+  upk2(ex2_fma2(pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f))), e0, e1);
+  e0 = (a0 < -126.f) ? 0.f : e0;
+  e1 = (a1 < -126.f) ? 0.f : e1;
+  const u64 e = pk2(e0, e1);
+  if (ORDER == 0) {
+    acc = add2(acc, e);
+    return;
+  }
+  acc = fma2(hermite_t<ORDER>(t), e, acc);
+}
+
+// fraction of pairs on the FMA-pipe exp for r = 4 (1 in 16, the LP optimum of
+// R (1 - phi) <= 16, R (7 + 8 phi) <= 128); 0 = MUFU only (default until measured)
+#ifndef PSI_HYB4
+#define PSI_HYB4 0
+#endif
+
 __device__ __forceinline__ Fx128 fx_from_double(double x) {
   Fx128 r;
   double fl = floor(x);
@@ -156,7 +185,10 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         pair2<ORDER, false>(j01, xi[k], s2[k], ph[k], acc[k]);
-        pair2<ORDER, false>(j23, xi[k], s2[k], ph[k], acc[k]);
+        if (PSI_HYB4 && ORDER == 4 && k == (q & (R - 1)) && (R >= 8 || (q & 1)))
+          pair2_fma<ORDER>(j23, xi[k], s2[k], ph[k], acc[k]);
+        else
+          pair2<ORDER, false>(j23, xi[k], s2[k], ph[k], acc[k]);
       }
     }
 #pragma unroll

@@ -56,4 +56,24 @@ __device__ __forceinline__ double f32_to_f64_alu(float f) {
   return __hiloint2double((int)hi, (int)lo);
 }
 
+// 2^a on the FMA pipe for two lanes, a in [-126, 0] (callers clamp): a = n + f with n = rint(a)
+// by the magic-number add (1.5 * 2^23), f in [-1/2, 1/2] exact, 2^f by a degree-5 minimax
+// polynomial (relative error 7.5e-8; 2.3e-7 with fp32 Horner), 2^n added to the exponent field
+// on the integer pipe.  8 FP32 lane-ops per lane (3 + 5 Horner) + 2 integer ops.
+__device__ __forceinline__ u64 ex2_fma2(u64 a) {
+  const u64 kMagic = 0x4B4000004B400000ull;  // 1.5 * 2^23
+  const u64 r = add2(a, kMagic);             // rint(a) in the low mantissa bits
+  const u64 f = sub2(a, sub2(r, kMagic));    // a - rint(a), exact
+  u64 q = fma2(0x3AAE04733AAE0473ull, f, 0x3C1E86293C1E8629ull);  // c5 f + c4
+  q = fma2(q, f, 0x3D635B723D635B72ull);     // + c3
+  q = fma2(q, f, 0x3E75FC8C3E75FC8Cull);     // + c2
+  q = fma2(q, f, 0x3F3172143F317214ull);     // + c1
+  q = fma2(q, f, 0x3F8000013F800001ull);     // + c0
+  float r0, r1, q0, q1;
+  upk2(r, r0, r1);
+  upk2(q, q0, q1);
+  return pk2(__uint_as_float(__float_as_uint(q0) + (__float_as_uint(r0) << 23)),
+             __uint_as_float(__float_as_uint(q1) + (__float_as_uint(r1) << 23)));
+}
+
 }  // namespace plg
