@@ -413,8 +413,8 @@ def kde_terms_visited(xh, h, pts, block=1024):
         p = pts[b:b + block].astype(np.float64)
         lo = np.searchsorted(xs, p.min() - cut, "left")
         hi = np.searchsorted(xs, p.max() + cut, "right")
-        tot += p.size * max(0, hi - lo)
-    return tot
+        tot += int(p.size) * max(0, int(hi - lo))
+    return int(tot)
 
 
 def run_kde(a):
