@@ -8,6 +8,8 @@
 // is deterministic.  LSD radix sort, 4 passes of 8 bits; each pass: per-tile digit
 // histograms, one exclusive scan, and a stable scatter (the tile is ordered by the
 // digit with 8 stable 1-bit splits in shared memory).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace plg {
@@ -136,10 +138,52 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const void* 
   }
 }
 
+// n <= kSortSmallMax: the whole sort in one CTA of 1024 threads -- ascending bitonic sort of the
+// radix keys in shared memory (pads 0xffffffff sort last), the same unique ascending array as
+// the 4-pass radix sort in 1 launch instead of 12 (the launches dominate at these sizes).
+constexpr int kSortSmallMax = 16384;
+__global__ void __launch_bounds__(1024) sort_small_kernel(const float* __restrict__ x, int64_t n, int npad,
+                                                          float* __restrict__ xs) {
+  extern __shared__ unsigned int key[];
+  for (int i = threadIdx.x; i < npad; i += 1024)
+    key[i] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (npad >> 1); i += 1024) {
+        const int lo = 2 * i - (i & (j - 1));  // lower index of the i-th pair at stride j
+        const int hi = lo + j;
+        const bool asc = (lo & k) == 0;
+        const unsigned int a = key[lo], b = key[hi];
+        if ((a > b) == asc) { key[lo] = b; key[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += 1024) reinterpret_cast<unsigned int*>(xs)[i] = key2bits(key[i]);
+}
+
 // x (float) -> xs (float, ascending).  tmp: n uint32; hist: 256*nb uint32.
 // Passes ping-pong tmp <-> xs (reinterpreted as keys); the last pass writes floats into xs.
 cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
                         int64_t nb, cudaStream_t s) {
+  static int force_radix = -1;  // PLUGIN_SORT_RADIX=1: always the 4-pass radix sort (testing)
+  if (force_radix < 0) {
+    const char* e = getenv("PLUGIN_SORT_RADIX");
+    force_radix = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (n <= kSortSmallMax && !force_radix) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sort_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(unsigned int) * kSortSmallMax));
+      attr = true;
+    }
+    int npad = 2;
+    while (npad < n) npad <<= 1;
+    sort_small_kernel<<<1, 1024, sizeof(unsigned int) * (size_t)npad, s>>>(x, n, npad, xs);
+    return cudaGetLastError();
+  }
   unsigned int* xk = reinterpret_cast<unsigned int*>(xs);
   const void* src = x;
   for (int pass = 0; pass < 4; ++pass) {

@@ -307,3 +307,20 @@ def test_fused_toy_data_bit_identical(P):
     b = P.read_result(P.plugin_h(x, flags=P.PLUGIN_MULTI_KERNEL))
     assert _same(a, b)
     assert rel(a["h"], 0.96146759322923324) < TOL   # SURVEY App. B.2 (50-digit value)
+
+
+def test_small_sort_matches_radix_sort_bit_for_bit(P):
+    # n <= 16384 sorts in one CTA (bitonic on the radix keys); PLUGIN_SORT_RADIX=1 forces the
+    # 4-pass radix sort: both give the same unique ascending array, hence identical results
+    import subprocess
+    import sys
+    code = ("import json, numpy as np, torch; from paper_1505_02100_b200 import plugin as P, inputs;"
+            "x = np.concatenate([inputs.mixture(9000, 12), np.array([0.0, -0.0, 1e-30, -1e-30] * 5, np.float32),"
+            " inputs.ties(3000, 1)]).astype(np.float32);"
+            "r = P.read_result(P.plugin_h(torch.from_numpy(x).cuda(), flags=P.PLUGIN_MULTI_KERNEL));"
+            "print(json.dumps({k: float(v).hex() for k, v in r.items()}))")
+    env = dict(__import__("os").environ)
+    a = subprocess.check_output([sys.executable, "-c", code], env=env, text=True).strip().splitlines()[-1]
+    env["PLUGIN_SORT_RADIX"] = "1"
+    b = subprocess.check_output([sys.executable, "-c", code], env=env, text=True).strip().splitlines()[-1]
+    assert a == b
