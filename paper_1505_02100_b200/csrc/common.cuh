@@ -33,7 +33,11 @@ constexpr int64_t kFusedMaxN = 4096;
 
 // rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
 int psi_rows_per_thread(int64_t n);
-inline int64_t psi_tile_edge(int64_t n) { return (int64_t)kPsiThreads * psi_rows_per_thread(n); }
+// R = 0: the small-tile mode of psi_tile.cuh (T = 64, n <= kFusedMaxN)
+inline int64_t psi_tile_edge(int64_t n) {
+  const int R = psi_rows_per_thread(n);
+  return R == 0 ? 64 : (int64_t)kPsiThreads * R;
+}
 inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
 

@@ -32,13 +32,13 @@ namespace plg {
 
 // min resident CTAs per SM for the register budget: R=8 -> 2 (<=128 regs), R<=4 -> 3 (<=80 regs)
 template <int R>
-struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : 3; };
+struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R == 0 ? 4 : 3); };
 
 template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
-  constexpr int T = kPsiThreads * R;
+  constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
@@ -86,7 +86,10 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
     } else {
       for (int q = tid; q < T; q += kPsiThreads) sx[q] = (q < jcount) ? __ldg(xs + j0 + q) : xpad;
     }
-    const double tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, (bi == bj) ? 1.0 : 2.0, red);
+    const double w = (bi == bj) ? 1.0 : 2.0;
+    double tt;
+    if constexpr (R == 0) tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+    else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
   }
@@ -100,10 +103,11 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
 }
 
 int psi_rows_per_thread(int64_t n) {
-  if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2 or 1)
+  if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2, 1; 0 = small tiles)
     int r = atoi(e);
-    if (r == 8 || r == 4 || r == 2 || r == 1) return r;
+    if (r == 8 || r == 4 || r == 2 || r == 1 || (r == 0 && n <= kFusedMaxN)) return r;
   }
+  if (n <= kFusedMaxN) return 0;  // small tiles (T = 64): latency-bound sizes
   // largest R in {8,4,2} whose tile count keeps >= ~28 tiles per resident CTA (296 on 148 SMs)
   const int cand[3] = {8, 4, 2};
   for (int c : cand) {
@@ -147,6 +151,7 @@ cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_hos
   PLG_CASE(4)
   PLG_CASE(2)
   PLG_CASE(1)
+  PLG_CASE(0)
 #undef PLG_CASE
 #undef PLG_ORDER
   return cudaErrorInvalidValue;

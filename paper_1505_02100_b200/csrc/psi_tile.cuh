@@ -240,4 +240,58 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
   return tt;
 }
 
+// Small tiles for small n (R = 0 in psi_rows_per_thread: n <= kFusedMaxN): T = 64 rows x 64
+// columns, thread tid takes row tid % 64 and the 16 columns 16 (tid / 64) .. + 15, so a pass
+// has 4x more, 16x smaller tiles than at T = 256 and spreads over the SMs (at these sizes the
+// pass is latency-bound).  Same pair arithmetic (pair2), dither and per-thread fp64 flush; the
+// result is valid in thread 0.  Contains __syncthreads().
+constexpr int kPsiSmallT = 64;
+
+template <int ORDER, bool LDG>
+__device__ __forceinline__ double psi_tile_sum_small(const float* sx, const float* __restrict__ xrows, int64_t n,
+                                                     int64_t i0, int jcount, float s, float xpad, double w,
+                                                     double* red) {
+  const int tid = threadIdx.x;
+  const int64_t i = i0 + (tid & (kPsiSmallT - 1));
+  const int jq = (tid >> 6) * 16;
+  const float v = (i < n) ? (LDG ? __ldg(xrows + i) : xrows[i]) : xpad;
+  const u64 xi = pk2(v, v);
+  const float p = row_phase(i);
+  const u64 ph = pk2(p, p);
+  const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+  const u64 s2 = pk2(si, si);
+  __syncthreads();
+  const float4* sx4 = reinterpret_cast<const float4*>(sx + jq);
+  u64 acc = 0ull;
+  if (jq + 16 <= jcount) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 t = sx4[q];
+      pair2<ORDER, false>(pk2(t.x, t.y), xi, s2, ph, acc);
+      pair2<ORDER, false>(pk2(t.z, t.w), xi, s2, ph, acc);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 t = sx4[q];
+      const int j = jq + 4 * q;
+      pair2<ORDER, true>(pk2(t.x, t.y), xi, s2, ph, acc, j < jcount, j + 1 < jcount);
+      pair2<ORDER, true>(pk2(t.z, t.w), xi, s2, ph, acc, j + 2 < jcount, j + 3 < jcount);
+    }
+  }
+  float a0, a1;
+  upk2(acc, a0, a1);
+  double tsum = (i < n) ? f32_to_f64_alu(a0 + a1) * exp2(-(double)p) : 0.0;
+  tsum *= w;
+  for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+  if ((tid & 31) == 0) red[tid >> 5] = tsum;
+  __syncthreads();
+  double tt = 0.0;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < kPsiThreads / 32; ++k) tt += red[k];
+  }
+  return tt;
+}
+
 }  // namespace plg
