@@ -435,18 +435,23 @@ def run_kde(a):
     for _ in range(a.warmup):
         P.kde_eval(x, h, p, out=f, ws=ws)
     torch.cuda.synchronize(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    def evs():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [evs() for _ in range(a.steps)]
     clk = ClockSampler(0)
     clk.start()
     time.sleep(0.3)
     for s in range(a.steps):
         flush.fill_(s & 0xff)
         ev[s][0].record(stream)
-        P.kde_eval(x, h, p, out=f, ws=ws)
-        ev[s][1].record(stream)
+        P.kde_prepare(x, ws)                                   # = kde_eval, split so the
+        ev[s][1].record(stream)                                #   kernel can be timed alone
+        P.kde_eval_prepared(n, h, p, ws, out=f)
+        ev[s][2].record(stream)
     torch.cuda.synchronize(dev)
     clocks = clk.stop()
-    ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in ev])
+    ms = statistics.median([e[0].elapsed_time(e[2]) for e in ev])
+    k_ms = statistics.median([e[1].elapsed_time(e[2]) for e in ev])
     visited = kde_terms_visited(xh, h, pts)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
@@ -455,7 +460,7 @@ def run_kde(a):
     # 1 of 4 with a 12-lane-op FMA-pipe exp2: min(16 / (3/4), 128 / (4 + 8/4)) = 21.33 terms/clk/SM
     per_clk = MUFU_EX2_PER_CLK_PER_SM if mufu_only else 64.0 / 3.0
     peak = per_clk * sms * f_meas * 1e6 / 1e9
-    achieved = visited / (ms / 1e3) / 1e9
+    achieved = visited / (k_ms / 1e3) / 1e9
     # end to end from host memory: H2D of X and the points, D2H of the curve
     xpin, ppin = torch.from_numpy(xh).pin_memory(), torch.from_numpy(pts).pin_memory()
     fh = torch.empty(m, dtype=torch.float64).pin_memory()
@@ -478,6 +483,7 @@ def run_kde(a):
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GTerms/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "kde_kernel",
+                         "kernel_ms": k_ms, "prepare_ms": ms - k_ms,
                          "peak_basis": (f"{per_clk:.2f} terms/clk/SM x {sms} SMs x {f_meas:.0f} MHz ("
                                         + ("MUFU.EX2-bound, 1 ex2 per visited term" if mufu_only else
                                            "MUFU + FMA pipes saturated together: 3/4 of the exps on MUFU.EX2, "

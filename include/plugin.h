@@ -226,6 +226,14 @@ size_t kde_workspace_bytes(int64_t n, int64_t m);
 plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_points, int64_t m,
                        double* d_f, void* d_ws, size_t ws_bytes, void* stream);
 
+/* kde_eval in two steps, for many point sets or bandwidths over one sample:
+ * kde_prepare sorts X into the workspace (and records whether it is all finite);
+ * kde_eval_prepared(n, h, ...) then evaluates on that workspace (same n, same results as
+ * kde_eval; the workspace must hold kde_workspace_bytes(n, m) for the largest m used). */
+plugin_status kde_prepare(const float* d_x, int64_t n, void* d_ws, size_t ws_bytes, void* stream);
+plugin_status kde_eval_prepared(int64_t n, double h, const float* d_points, int64_t m, double* d_f,
+                                void* d_ws, size_t ws_bytes, void* stream);
+
 /* Text of the last non-OK return on this thread ("" if none).  Static storage. */
 const char* plugin_last_error(void);
 

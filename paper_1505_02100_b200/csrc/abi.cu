@@ -346,20 +346,23 @@ size_t kde_workspace_bytes(int64_t n, int64_t m) {
   return layout(n).total + kde_extra_bytes(n, m);
 }
 
-plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_points, int64_t m, double* d_f,
-                       void* d_ws, size_t ws_bytes, void* stream) {
-  g_err[0] = 0;
+static plugin_status kde_check(int64_t n, double h, const float* d_points, int64_t m, double* d_f) {
   plugin_status st = check_n(n, 1);
   if (st != PLUGIN_OK) return st;
   if (m < 0 || m > kMaxN) return fail(PLUGIN_E_INVALID, "m out of range%s (m=%lld)", "", (long long)m);
-  if (!d_x || (m > 0 && (!d_points || !d_f))) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  if (m > 0 && (!d_points || !d_f)) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   // h must be finite, > 0 and keep -log2(e)/(2 h^2) a normal float32
   if (!(std::isfinite(h) && h >= 1e-18 && h <= 1e18)) return fail(PLUGIN_E_INVALID, "h must be in [1e-18, 1e18]%s");
-  if (m == 0) return PLUGIN_OK;
+  return PLUGIN_OK;
+}
+
+plugin_status kde_prepare(const float* d_x, int64_t n, void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_x) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
   WS w;
   if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
-  if (ws_bytes < kde_workspace_bytes(n, m))
-    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)kde_workspace_bytes(n, m));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
   if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
@@ -367,9 +370,36 @@ plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_poi
   // Step I reduction only for its non-finite flag (a NaN/Inf sample makes every f NaN)
   plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
-  void* extra = static_cast<char*>(d_ws) + w.L.total;
-  if ((e = launch_kde(w.xs, n, h, d_points, m, w.ctrl, extra, d_f, s)) != cudaSuccess) return cuda_fail(e, "kde");
   return PLUGIN_OK;
+}
+
+plugin_status kde_eval_prepared(int64_t n, double h, const float* d_points, int64_t m, double* d_f, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  plugin_status st = kde_check(n, h, d_points, m, d_f);
+  if (st != PLUGIN_OK) return st;
+  if (m == 0) return PLUGIN_OK;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  if (ws_bytes < kde_workspace_bytes(n, m))
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)kde_workspace_bytes(n, m));
+  void* extra = static_cast<char*>(d_ws) + w.L.total;
+  cudaError_t e = launch_kde(w.xs, n, h, d_points, m, w.ctrl, extra, d_f, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "kde");
+  return PLUGIN_OK;
+}
+
+plugin_status kde_eval(const float* d_x, int64_t n, double h, const float* d_points, int64_t m, double* d_f,
+                       void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  plugin_status st = kde_check(n, h, d_points, m, d_f);
+  if (st != PLUGIN_OK) return st;
+  if (!d_x) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  if (m == 0) return PLUGIN_OK;
+  if (ws_bytes < kde_workspace_bytes(n, m))
+    return fail(PLUGIN_E_INVALID, "workspace too small%s: need %lld bytes", "", (long long)kde_workspace_bytes(n, m));
+  if ((st = kde_prepare(d_x, n, d_ws, ws_bytes, stream)) != PLUGIN_OK) return st;
+  return kde_eval_prepared(n, h, d_points, m, d_f, d_ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -88,6 +88,8 @@ def lib():
             "plugin_h_q32": (i32, [P, i64, P, P, sz, P]),
             "kde_workspace_bytes": (sz, [i64, i64]),
             "kde_eval": (i32, [P, i64, d, P, i64, P, P, sz, P]),
+            "kde_prepare": (i32, [P, i64, P, sz, P]),
+            "kde_eval_prepared": (i32, [i64, d, P, i64, P, P, sz, P]),
             "plugin_last_error": (ctypes.c_char_p, []),
             "plugin_version": (ctypes.c_char_p, []),
         }
@@ -105,7 +107,8 @@ PLUGIN_MULTI_KERNEL = 2
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
             "plugin_shard_tiles", "plugin_dpi", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
-            "kde_workspace_bytes", "kde_eval", "plugin_last_error", "plugin_version")
+            "kde_workspace_bytes", "kde_eval", "kde_prepare",
+            "kde_eval_prepared", "plugin_last_error", "plugin_version")
 
 
 def _check(st: int):
@@ -305,6 +308,23 @@ def kde_eval(x: torch.Tensor, h: float, points: torch.Tensor, out: torch.Tensor 
     out = torch.empty(m, dtype=torch.float64, device=x.device) if out is None else out
     _check(lib().kde_eval(x.data_ptr(), n, float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(),
                           ws.numel(), _stream(stream)))
+    return out
+
+
+def kde_prepare(x: torch.Tensor, ws: torch.Tensor, stream=None) -> torch.Tensor:
+    """Sort X into the KDE workspace once (then kde_eval_prepared for any points / h)."""
+    x = _x(x)
+    _check(lib().kde_prepare(x.data_ptr(), x.numel(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return ws
+
+
+def kde_eval_prepared(n: int, h: float, points: torch.Tensor, ws: torch.Tensor, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    points = _x(points)
+    m = points.numel()
+    out = torch.empty(m, dtype=torch.float64, device=points.device) if out is None else out
+    _check(lib().kde_eval_prepared(int(n), float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   _stream(stream)))
     return out
 
 

@@ -140,3 +140,14 @@ def test_kde_full_size_sampled_points(P, oracle_mod, k):
     # unit mass of the whole curve (trapezoid)
     mass = float(np.sum((got[1:] + got[:-1]) * np.diff(pts.astype(np.float64))) / 2)
     assert mass == pytest.approx(1.0, abs=1e-4)
+
+
+def test_kde_prepare_then_eval_equals_kde_eval(P):
+    x = torch.from_numpy(inputs.mixture(40000, 9)).cuda()
+    pts = torch.linspace(-7, 7, 3001, device="cuda")
+    a = P.kde_eval(x, 0.12, pts).cpu()
+    ws = P.kde_workspace(x.numel(), pts.numel(), x.device)
+    P.kde_prepare(x, ws)
+    b = P.kde_eval_prepared(x.numel(), 0.12, pts, ws).cpu()
+    c = P.kde_eval_prepared(x.numel(), 0.12, pts[:1000].contiguous(), ws).cpu()   # re-use
+    assert torch.equal(a, b) and torch.equal(a[:1000], c)
