@@ -150,4 +150,6 @@ def test_kde_prepare_then_eval_equals_kde_eval(P):
     P.kde_prepare(x, ws)
     b = P.kde_eval_prepared(x.numel(), 0.12, pts, ws).cpu()
     c = P.kde_eval_prepared(x.numel(), 0.12, pts[:1000].contiguous(), ws).cpu()   # re-use
-    assert torch.equal(a, b) and torch.equal(a[:1000], c)
+    assert torch.equal(a, b)
+    # another point set: other windows and segment splits, the same values to fp64 rounding
+    assert torch.allclose(a[:1000], c, rtol=1e-12, atol=0)
