@@ -151,5 +151,6 @@ def test_kde_prepare_then_eval_equals_kde_eval(P):
     b = P.kde_eval_prepared(x.numel(), 0.12, pts, ws).cpu()
     c = P.kde_eval_prepared(x.numel(), 0.12, pts[:1000].contiguous(), ws).cpu()   # re-use
     assert torch.equal(a, b)
-    # another point set: other windows and segment splits, the same values to fp64 rounding
-    assert torch.allclose(a[:1000], c, rtol=1e-12, atol=0)
+    # another point set: other windows, segment splits and fp32 chunks -- equal within the
+    # fp32 evaluation tolerance of this file
+    assert torch.allclose(a[:1000], c, rtol=5e-6, atol=0)
