@@ -55,6 +55,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
   __shared__ int sh_bad[8];
   __shared__ double p1[2 * 8];
   __shared__ plugin_result res;
+  __shared__ Fx128 fx_red[kPsiThreads / 32];
   constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
   unsigned int* key = reinterpret_cast<unsigned int*>(xsm);
   const int tid = threadIdx.x;
@@ -119,10 +120,23 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
     }
     grid.sync();
     if (ok) {
+      // every CTA adds all the partials: in parallel over the threads (independent L2 loads),
+      // then a 128-bit shuffle / shared-memory reduction -- integer addition, so any order
+      // gives the same total
+      Fx128 tot = {0ull, 0ll};
+      for (unsigned int b = tid; b < gridDim.x; b += kPsiThreads) fx_add(tot, ldcg_fx(parts + pass * gridDim.x + b));
+      for (int o = 16; o; o >>= 1) {
+        Fx128 other;
+        other.lo = __shfl_xor_sync(0xffffffffu, tot.lo, o);
+        other.hi = __shfl_xor_sync(0xffffffffu, tot.hi, o);
+        fx_add(tot, other);
+      }
+      if ((tid & 31) == 0) fx_red[tid >> 5] = tot;
+      __syncthreads();
       if (tid == 0) {
-        Fx128 tot = {0ull, 0ll};
-        for (unsigned int b = 0; b < gridDim.x; ++b) fx_add(tot, ldcg_fx(parts + pass * gridDim.x + b));
-        finalize_pass(pass, fx_to_double(tot), n, &res);
+        Fx128 all = {0ull, 0ll};
+        for (int w = 0; w < kPsiThreads / 32; ++w) fx_add(all, fx_red[w]);
+        finalize_pass(pass, fx_to_double(all), n, &res);
       }
       __syncthreads();
     }
