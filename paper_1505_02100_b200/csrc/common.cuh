@@ -55,10 +55,10 @@ struct Fx128 { unsigned long long lo; long long hi; };
 // ---- workspace layout ----------------------------------------------------------
 struct Ctrl {                       // zeroed at the start of every API call
   Fx128 acc[2];                     // psi accumulators (slot 0: r=6, slot 1: r=4 / psi_r)
-  unsigned int tile_counter[2];     // dynamic tile scheduler per slot
+  unsigned long long tile_counter[2];  // dynamic tile scheduler per slot (64-bit: n^2 tiles can pass 2^32)
   unsigned int step1_done;          // last-block-done counter of Step I
   int nonfinite;                    // set if any X is NaN/Inf
-  unsigned int pad[58];
+  unsigned int pad[56];
 };
 static_assert(sizeof(Ctrl) <= 512, "ctrl block");
 

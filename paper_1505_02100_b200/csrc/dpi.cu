@@ -73,7 +73,7 @@ __global__ void dpi_finalize_kernel(Ctrl* ctrl, int slot, int j, plugin_dpi_resu
   const Fx128 acc = ctrl->acc[slot];
   ctrl->acc[slot].lo = 0ull;  // reset for the next pass on this workspace
   ctrl->acc[slot].hi = 0ll;
-  ctrl->tile_counter[slot] = 0u;
+  ctrl->tile_counter[slot] = 0ull;
   if (out->status != PLUGIN_OK) return;
   const int r = 2 * j + 2;
   const double nd = (double)out->n;

@@ -57,7 +57,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   const int tid = threadIdx.x;
 
   for (;;) {
-    if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1u);
+    if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
     __syncthreads();
     const int64_t t = s_tile;
     if (t >= tile_end) break;

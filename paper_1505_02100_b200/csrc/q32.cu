@@ -84,7 +84,7 @@ psi_q32_kernel(const long long* __restrict__ zq, int64_t n, long long rg_host, c
   const int64_t nb = (n + kQ32T - 1) / kQ32T, tiles = nb * (nb + 1) / 2;
   Fx128 cta = {0ull, 0ll};
   for (;;) {
-    if (tid == 0) s_tile = (long long)atomicAdd(&ctrl->tile_counter[slot], 1u);
+    if (tid == 0) s_tile = (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
     __syncthreads();
     const int64_t t = s_tile;
     if (t >= tiles) break;
@@ -158,7 +158,7 @@ __global__ void q32_finalize_kernel(Ctrl* ctrl, int slot, long long* out, int wh
   const Fx128 acc = ctrl->acc[slot];
   ctrl->acc[slot].lo = 0ull;
   ctrl->acc[slot].hi = 0ll;
-  ctrl->tile_counter[slot] = 0u;
+  ctrl->tile_counter[slot] = 0ull;
   if (out) {
     out[0] = (long long)acc.lo;
     out[1] = acc.hi;

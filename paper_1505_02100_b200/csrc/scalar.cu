@@ -73,7 +73,7 @@ __global__ void finalize_kernel(int what, Ctrl* ctrl, int slot, const plugin_fx1
     // reset for the next pass on this workspace
     ctrl->acc[slot].lo = 0ull;
     ctrl->acc[slot].hi = 0ll;
-    ctrl->tile_counter[slot] = 0u;
+    ctrl->tile_counter[slot] = 0ull;
   }
   if (total) acc = limbs_to_fx(total);
   if (n <= 0 && out) n = out->n;
