@@ -71,6 +71,15 @@ def main():
             P.plugin_h(x, out=out, ws=ws, flags=P.PLUGIN_MULTI_KERNEL)
         med, mn = dev_time(g.replay, a.reps)
         row["graph_multi_kernel_us"], row["graph_multi_kernel_min_us"] = med, mn
+        # the default path (one cooperative launch for n <= 4096) captured in a graph too
+        try:
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2):
+                P.plugin_h(x, out=out, ws=ws)
+            med, mn = dev_time(g2.replay, a.reps)
+            row["graph_default_us"], row["graph_default_min_us"] = med, mn
+        except Exception as e:  # report, do not hide: the header claims capturability
+            row["graph_default_error"] = repr(e)
         row["h"] = h_default
         row["same_h_all_paths"] = P.read_result(out)["h"] == h_default
         xpin = torch.from_numpy(xh).pin_memory()
