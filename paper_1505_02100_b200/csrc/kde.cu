@@ -73,8 +73,13 @@ __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
   return lo;
 }
 
+// resident CTAs per SM the register budget is sized for (tuning: -DKDE_OCC=3 fits 78 registers)
+#ifndef KDE_OCC
+#define KDE_OCC 2
+#endif
+
 template <bool HYB>
-__global__ void __launch_bounds__(kKdeThreads, 2)
+__global__ void __launch_bounds__(kKdeThreads, KDE_OCC)
 kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pts, int64_t m, float kf, double cut,
            int S, double scale, const Ctrl* ctrl, double* __restrict__ partial, unsigned int* __restrict__ counters,
            double* __restrict__ f) {
