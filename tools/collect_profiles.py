@@ -62,7 +62,8 @@ def main():
     for f in sorted(glob.glob(os.path.join(OUT, "bench*.json"))):
         if os.path.getsize(f):
             shutil.copy(f, os.path.join(PROF, f"{tag}_{os.path.basename(f)}"))
-    for f in ("latency.jsonl", "pytest_gpu.log", "entry_smoke.log", "smoke.log"):
+    for f in ("latency.jsonl", "pytest_gpu.log", "entry_smoke.log", "smoke.log", "parity_report.jsonl", "ab.log",
+              "oracle_cfg5.log"):
         p = os.path.join(OUT, f)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(PROF, f"{tag}_{f}"))
