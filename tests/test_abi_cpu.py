@@ -77,3 +77,16 @@ def test_kde_workspace_sizing(L):
             assert b >= base and b % 256 == 0
             nb = -(-m // 1024)
             assert b <= base + 8 * 1024 * (8 * 148 + nb) + 4 * nb + 512
+
+
+def test_cli_loader_formats(tmp_path):
+    import numpy as np
+
+    from paper_1505_02100_b200.__main__ import _load
+    x = np.array([0.0, 1.0, 1.1, 1.5, 1.9, 2.8, 2.9, 3.5])           # the toy data of P:51
+    np.save(tmp_path / "a.npy", x)
+    x.astype("<f4").tofile(tmp_path / "a.f32")
+    np.savetxt(tmp_path / "a.txt", x)
+    for f in ("a.npy", "a.f32", "a.txt"):
+        got = _load(str(tmp_path / f))
+        assert got.dtype == np.float32 and np.array_equal(got, x.astype(np.float32))

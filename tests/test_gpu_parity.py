@@ -324,3 +324,19 @@ def test_small_sort_matches_radix_sort_bit_for_bit(P):
     env["PLUGIN_SORT_RADIX"] = "1"
     b = subprocess.check_output([sys.executable, "-c", code], env=env, text=True).strip().splitlines()[-1]
     assert a == b
+
+
+def test_cli_bandwidth_and_compare(P, tmp_path):
+    import json
+    import subprocess
+    import sys
+    x = inputs.TOY.astype(np.float32)
+    np.save(tmp_path / "toy.npy", x)
+    out = subprocess.check_output([sys.executable, "-m", "paper_1505_02100_b200", "compare", str(tmp_path / "toy.npy"),
+                                   "--h-ref", "0.96146759322923324"], text=True)
+    r = json.loads(out.strip().splitlines()[-1])
+    assert r["status"] == 0 and r["rel_diff"] < TOL
+    out = subprocess.check_output([sys.executable, "-m", "paper_1505_02100_b200", "kde", str(tmp_path / "toy.npy"),
+                                   "--h", str(r["h"]), "--grid", "-5", "8.5", "4001"], text=True)
+    k = json.loads(out.strip().splitlines()[-1])
+    assert abs(k["trapezoid_mass"] - 1.0) < 1e-3
