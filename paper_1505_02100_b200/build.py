@@ -53,6 +53,21 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return lib_path
 
 
+EXAMPLE = os.path.join(ROOT, "examples", "plugin_h_example")
+
+
+def build_example() -> str:
+    """The plain-C user of the ABI (examples/plugin_h_example.c), linked against libplugin.so."""
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+           EXAMPLE + ".c", "-L", HERE, "-lplugin", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           f"-Wl,-rpath,{HERE}", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", EXAMPLE]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"example build failed:\n{p.stdout}\n{p.stderr}")
+    return EXAMPLE
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

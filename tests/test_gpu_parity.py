@@ -340,3 +340,19 @@ def test_cli_bandwidth_and_compare(P, tmp_path):
                                    "--h", str(r["h"]), "--grid", "-5", "8.5", "4001"], text=True)
     k = json.loads(out.strip().splitlines()[-1])
     assert abs(k["trapezoid_mass"] - 1.0) < 1e-3
+
+
+def test_plain_c_example_uses_the_abi(P, tmp_path):
+    # examples/plugin_h_example.c: the C ABI from plain C (no Python, no torch on its path)
+    import json
+    import subprocess
+    exe = os.path.join(os.path.dirname(HERE), "examples", "plugin_h_example")
+    assert os.path.exists(exe), "built by __graft_entry__.build()"
+    r = json.loads(subprocess.check_output([exe], text=True))
+    assert r["status"] == 0 and rel(r["h"], 0.96146759322923324) < TOL       # toy data, SURVEY App. B.2
+    x = inputs.config_data(1)
+    x.astype("<f4").tofile(tmp_path / "cfg1.f32")
+    r = json.loads(subprocess.check_output([exe, str(tmp_path / "cfg1.f32")], text=True))
+    g = _golden(1)
+    for k in ("psi6", "psi4", "h"):
+        assert rel(r[k], g[k]) < TOL
