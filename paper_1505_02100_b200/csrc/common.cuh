@@ -29,7 +29,7 @@ inline __host__ __device__ int step1_grid(int64_t n) {
   return (int)(want < kStep1Blocks ? (want < 1 ? 1 : want) : kStep1Blocks);
 }
 // the fused single-launch path (fused.cu) handles n up to this
-constexpr int64_t kFusedMaxN = 4096;
+constexpr int64_t kFusedMaxN = 2048;
 
 // rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
 int psi_rows_per_thread(int64_t n);

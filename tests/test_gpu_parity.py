@@ -271,9 +271,9 @@ def _same(a, b):
     return all(a[k] == b[k] or (isinstance(a[k], float) and math.isnan(a[k]) and math.isnan(b[k])) for k in a)
 
 
-@pytest.mark.parametrize("n", [2, 3, 31, 255, 256, 257, 1000, 1024, 1025, 2049, 4096])
+@pytest.mark.parametrize("n", [2, 3, 31, 63, 64, 65, 255, 256, 257, 1000, 1024, 1025, 2047, 2048, 2049, 4096])
 def test_fused_small_n_bit_identical_to_multi_kernel(P, oracle_mod, n):
-    # n <= 4096: plugin_h runs one cooperative launch (fused.cu); it must reproduce the
+    # n <= 2048: plugin_h runs one cooperative launch (fused.cu); it must reproduce the
     # multi-kernel sequence bit for bit, and both must match the oracle
     x = inputs.mixture(n, 300 + n) if n > 3 else inputs.normal(n, 300 + n)
     xt = torch.from_numpy(x).cuda()
