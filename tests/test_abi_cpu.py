@@ -90,3 +90,16 @@ def test_cli_loader_formats(tmp_path):
     for f in ("a.npy", "a.f32", "a.txt"):
         got = _load(str(tmp_path / f))
         assert got.dtype == np.float32 and np.array_equal(got, x.astype(np.float32))
+
+
+@pytest.mark.parametrize("lang", ["c", "c++"])
+def test_header_is_self_contained_c_and_cpp(tmp_path, lang):
+    # include/plugin.h is the boundary: it must compile on its own as C11 and as C++
+    import subprocess
+    src = tmp_path / ("t.c" if lang == "c" else "t.cpp")
+    src.write_text('#include "plugin.h"\nint main(void) { plugin_result r; (void)r; return (int)sizeof(plugin_fx128); }\n')
+    cc = "gcc" if lang == "c" else "g++"
+    std = "-std=c11" if lang == "c" else "-std=c++17"
+    p = subprocess.run([cc, std, "-Wall", "-Werror", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
