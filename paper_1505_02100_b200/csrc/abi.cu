@@ -40,7 +40,7 @@ Layout layout(int64_t n) {
   L.result = off;
   off = align_up(off + sizeof(plugin_result), 256);
   L.fused = off;
-  off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid, 256);  // fused.cu partials (32 KB)
+  off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid + 256, 256);  // fused.cu partials (32 KB) + timing slots
   L.total = off;
   return L;
 }

@@ -23,6 +23,23 @@ namespace cg = cooperative_groups;
 
 namespace plg {
 
+// -DPLUGIN_FUSED_TIMING: CTA 0 records %globaltimer (ns) at the phase boundaries into the
+// workspace after the partials (tools/fused_phases.py reads them); off in the product build
+#ifdef PLUGIN_FUSED_TIMING
+#define FT_MARK(k)                                                                   \
+  do {                                                                               \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                       \
+      unsigned long long t;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                          \
+      reinterpret_cast<unsigned long long*>(parts + 2 * kFusedMaxGrid)[k] = t;       \
+    }                                                                                \
+  } while (0)
+#else
+#define FT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 // ascending bitonic sort of npad (a power of two) keys in shared memory, whole CTA
 __device__ __forceinline__ void cta_bitonic_sort(unsigned int* key, int npad) {
   for (int k = 2; k <= npad; k <<= 1) {
@@ -60,11 +77,13 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
   unsigned int* key = reinterpret_cast<unsigned int*>(xsm);
   const int tid = threadIdx.x;
 
+  FT_MARK(0);
   // sort (keys of the raw bits: pads are 0xffffffff and sort last)
   for (int i = tid; i < npad; i += kPsiThreads)
     key[i] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
   __syncthreads();
   cta_bitonic_sort(key, npad);
+  FT_MARK(1);
   for (int i = tid; i < n; i += kPsiThreads) key[i] = key2bits(key[i]);
   __syncthreads();
   const float xpad = xsm[n - 1];
@@ -90,6 +109,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
   }
   __syncthreads();
 
+  FT_MARK(2);
   // Steps IV/V and VI/VII
   cg::grid_group grid = cg::this_grid();
   const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
@@ -118,7 +138,9 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
       }
       if (tid == 0) parts[pass * gridDim.x + blockIdx.x] = acc;
     }
+    FT_MARK(3 + 3 * pass);
     grid.sync();
+    FT_MARK(4 + 3 * pass);
     if (ok) {
       // every CTA adds all the partials: in parallel over the threads (independent L2 loads),
       // then a 128-bit shuffle / shared-memory reduction -- integer addition, so any order
@@ -140,6 +162,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
       }
       __syncthreads();
     }
+    FT_MARK(5 + 3 * pass);
   }
   if (blockIdx.x == 0 && tid == 0) *out = res;
 }
