@@ -18,7 +18,8 @@
 
 namespace plg {
 
-constexpr int kQ32R = 4;
+constexpr int kQ32R = 1;  // T = 256: at ~20 128-bit multiplies per pair even small tiles carry ample work,
+                             // and n = 16384 still gets 2080 tiles to spread over the SMs
 constexpr int kQ32T = kPsiThreads * kQ32R;
 
 __device__ __forceinline__ long long q32_mul(long long a, long long b) {
