@@ -1,5 +1,5 @@
 // fused.cu -- the whole of Algorithm 1 in ONE cooperative launch for
-// small samples (n <= kFusedMaxN = 4096, which covers the paper's own workloads n = 128..1024
+// small samples (n <= kFusedMaxN = 2048, which covers the paper's own workloads n = 128..1024
 // of Tables 2-4 and BASELINE config 1).  At these sizes a pass is ~0.1-4 us of arithmetic, so
 // the 20 launches of the multi-kernel path dominate; here they become one launch and two
 // grid-wide barriers.
@@ -73,7 +73,8 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
   __shared__ double p1[2 * 8];
   __shared__ plugin_result res;
   __shared__ Fx128 fx_red[kPsiThreads / 32];
-  constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
+  static_assert(R == 0, "the fused path uses the small tiles of psi_tile.cuh");
+  constexpr int T = kPsiSmallT;
   unsigned int* key = reinterpret_cast<unsigned int*>(xsm);
   const int tid = threadIdx.x;
 
@@ -127,13 +128,8 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
           continue;  // all terms exactly zero (psi.cu); uniform across the CTA
         const int jcount = (int)((n - j0) < T ? (n - j0) : T);
         const double w = (bi == bj) ? 1.0 : 2.0;
-        double tt;
-        if constexpr (R == 0)
-          tt = (pass == 0) ? psi_tile_sum_small<6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
-                           : psi_tile_sum_small<4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
-        else
-          tt = (pass == 0) ? psi_tile_sum<R, 6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
-                           : psi_tile_sum<R, 4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
+        const double tt = (pass == 0) ? psi_tile_sum_small<6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
+                                      : psi_tile_sum_small<4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
         if (tid == 0) fx_add(acc, fx_from_double(tt));
       }
       if (tid == 0) parts[pass * gridDim.x + blockIdx.x] = acc;
@@ -168,36 +164,32 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
 }
 
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {
-  const int R = psi_rows_per_thread(n);
-  if (n < 2 || n > kFusedMaxN || (R != 0 && R != 1)) return cudaErrorNotSupported;
-  static int max_grid[2] = {-1, -1};
-  const int which = R;  // 0: small tiles (default), 1: T = 256 (PLUGIN_PSI_R=1)
-  const void* fn = which == 0 ? (const void*)plugin_fused_kernel<0> : (const void*)plugin_fused_kernel<1>;
-  if (max_grid[which] < 0) {
+  if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n) != 0) return cudaErrorNotSupported;
+  static int max_grid = -1;
+  if (max_grid < 0) {
     int dev = 0, sms = 0, occ = 0, coop = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (which == 0)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<0>, kPsiThreads, sizeof(float) * kFusedMaxN);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<1>, kPsiThreads, sizeof(float) * kFusedMaxN);
-    max_grid[which] = coop ? sms * occ : 0;
-    if (max_grid[which] > kFusedMaxGrid) max_grid[which] = kFusedMaxGrid;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<0>, kPsiThreads,
+                                                  sizeof(float) * kFusedMaxN);
+    max_grid = coop ? sms * occ : 0;
+    if (max_grid > kFusedMaxGrid) max_grid = kFusedMaxGrid;
   }
-  if (max_grid[which] <= 0) return cudaErrorNotSupported;
+  if (max_grid <= 0) return cudaErrorNotSupported;
   int npad = 2;
   while (npad < n) npad <<= 1;
-  const int64_t T = which == 0 ? kPsiSmallT : kPsiThreads, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
+  const int64_t T = kPsiSmallT, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
   int nsx = (int)(nb * T > npad ? nb * T : npad);
   // one CTA per SM at most: every CTA sorts its own copy of X, so more CTAs than SMs add no speed
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int grid = (int)(tiles < max_grid[which] ? tiles : max_grid[which]);
+  int grid = (int)(tiles < max_grid ? tiles : max_grid);
   if (grid > sms) grid = sms;
   size_t smem = sizeof(float) * (size_t)nsx;
   void* args[] = {(void*)&x, (void*)&n, (void*)&npad, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPsiThreads), args, smem, s);
+  return cudaLaunchCooperativeKernel((const void*)plugin_fused_kernel<0>, dim3(grid), dim3(kPsiThreads), args, smem,
+                                     s);
 }
 
 }  // namespace plg

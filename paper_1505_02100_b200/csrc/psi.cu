@@ -76,20 +76,29 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       }
     }
     const int jcount = (int)((n - j0) < T ? (n - j0) : T);
+    // tile centre (R >= 1 tiles, PSI_CENTER): the first row's value; sx holds fl(x_j - cen)
+    const float cen = (R > 0 && PSI_CENTER) ? __ldg(xs + i0) : 0.f;
     // stage the tile's j values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
     if (jcount == T) {
       const float4* src = reinterpret_cast<const float4*>(xs + j0);
       float4* dst = reinterpret_cast<float4*>(sx);
 #pragma unroll
-      for (int q = 0; q < T / 4 / kPsiThreads; ++q) dst[q * kPsiThreads + tid] = __ldg(src + q * kPsiThreads + tid);
-      if (T / 4 < kPsiThreads && tid < T / 4) dst[tid] = __ldg(src + tid);
+      for (int q = 0; q < T / 4 / kPsiThreads; ++q) {
+        float4 v = __ldg(src + q * kPsiThreads + tid);
+        v.x = __fsub_rn(v.x, cen);
+        v.y = __fsub_rn(v.y, cen);
+        v.z = __fsub_rn(v.z, cen);
+        v.w = __fsub_rn(v.w, cen);
+        dst[q * kPsiThreads + tid] = v;
+      }
+      if (T / 4 < kPsiThreads && tid < T / 4) dst[tid] = __ldg(src + tid);  // R = 0 (cen = 0)
     } else {
-      for (int q = tid; q < T; q += kPsiThreads) sx[q] = (q < jcount) ? __ldg(xs + j0 + q) : xpad;
+      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + j0 + q) : xpad, cen);
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
     if constexpr (R == 0) tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
-    else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+    else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
   }

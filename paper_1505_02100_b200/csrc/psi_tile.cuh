@@ -70,11 +70,13 @@ __device__ __forceinline__ u64 hermite_t(u64 t) {
   return p;
 }
 
-template <int ORDER, bool MASK>
+// CENTER = false: xj, xi are raw sample values, u = (x_j - x_i) s (difference first).
+// CENTER = true (PSI_CENTER): xj = fl(x_j - c) and xi = -fl(fl(x_i - c) s) for a tile centre c
+// (the tile's first row), u = fma(xj, s, xi): one FP32 op instead of two.
+template <int ORDER, bool MASK, bool CENTER = false>
 __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, bool m0 = true, bool m1 = true) {
   const u64 c2 = 0xBF38AA3BBF38AA3Bull;  // {fp32(-log2(e)/2)} x 2 = -0.72134752f
-  u64 d = sub2(xj, xi);
-  u64 u = mul2(d, s2);
+  u64 u = CENTER ? fma2(xj, s2, xi) : mul2(sub2(xj, xi), s2);
   u64 t = mul2(u, u);
   u64 a = fma2(t, c2, ph);
   float a0, a1;
@@ -91,35 +93,6 @@ __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, 
   }
   acc = fma2(hermite_t<ORDER>(t), e, acc);
 }
-
-// pair2 with the exp on the FMA pipe (ex2_fma2) instead of MUFU.EX2 (PSI_HYB4): results below
-// 2^-126 are set to +0 as MUFU.EX2.ftz flushes them, so all-zero tiles stay exactly zero.
-template <int ORDER>
-__device__ __forceinline__ void pair2_fma(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc) {
-  const u64 c2 = 0xBF38AA3BBF38AA3Bull;
-  u64 d = sub2(xj, xi);
-  u64 u = mul2(d, s2);
-  u64 t = mul2(u, u);
-  u64 a = fma2(t, c2, ph);
-  float a0, a1;
-  upk2(a, a0, a1);
-  float e0, e1;
-  upk2(ex2_fma2(pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f))), e0, e1);
-  e0 = (a0 < -126.f) ? 0.f : e0;
-  e1 = (a1 < -126.f) ? 0.f : e1;
-  const u64 e = pk2(e0, e1);
-  if (ORDER == 0) {
-    acc = add2(acc, e);
-    return;
-  }
-  acc = fma2(hermite_t<ORDER>(t), e, acc);
-}
-
-// fraction of pairs on the FMA-pipe exp for r = 4 (1 in 16, the LP optimum of
-// R (1 - phi) <= 16, R (7 + 8 phi) <= 128); 0 = MUFU only (default until measured)
-#ifndef PSI_HYB4
-#define PSI_HYB4 0
-#endif
 
 __device__ __forceinline__ Fx128 fx_from_double(double x) {
   Fx128 r;
@@ -153,10 +126,17 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
 //   xrows : the sorted sample, rows i0 .. i0 + T - 1 (i >= n reads as xpad and is dropped)
 //   red   : shared scratch of kPsiThreads / 32 doubles
 // Called by all 256 threads; the result is valid in thread 0.  Contains __syncthreads().
+#ifndef PSI_CENTER
+#define PSI_CENTER 1
+#endif
+
+// cen: the tile centre when PSI_CENTER (sx then holds fl(x_j - cen)); ignored otherwise
 template <int R, int ORDER, bool LDG>
 __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __restrict__ xrows, int64_t n, int64_t i0,
-                                               int jcount, float s, float xpad, double w, double* red) {
+                                               int jcount, float s, float xpad, double w, double* red,
+                                               float cen = 0.f) {
   constexpr int CH = PSI_CH;  // j per fp32 chunk (CH/2 per packed lane) before the fp64 flush
+  constexpr bool CEN = PSI_CENTER != 0;
   const int tid = threadIdx.x;
   u64 xi[R], ph[R], s2[R];
   double drow[R];
@@ -164,10 +144,11 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
   for (int k = 0; k < R; ++k) {
     const int64_t i = i0 + k * kPsiThreads + tid;
     const float v = (i < n) ? (LDG ? __ldg(xrows + i) : xrows[i]) : xpad;
-    xi[k] = pk2(v, v);
+    const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+    const float vi = CEN ? -__fmul_rn(__fsub_rn(v, cen), si) : v;
+    xi[k] = pk2(vi, vi);
     const float p = row_phase(i);
     ph[k] = pk2(p, p);
-    const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
     s2[k] = pk2(si, si);
     drow[k] = 0.0;
   }
@@ -184,11 +165,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
       const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        pair2<ORDER, false>(j01, xi[k], s2[k], ph[k], acc[k]);
-        if (PSI_HYB4 && ORDER == 4 && k == (q & (R - 1)) && (R >= 8 || (q & 1)))
-          pair2_fma<ORDER>(j23, xi[k], s2[k], ph[k], acc[k]);
-        else
-          pair2<ORDER, false>(j23, xi[k], s2[k], ph[k], acc[k]);
+        pair2<ORDER, false, CEN>(j01, xi[k], s2[k], ph[k], acc[k]);
+        pair2<ORDER, false, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
       }
     }
 #pragma unroll
@@ -209,8 +187,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
       const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        pair2<ORDER, true>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
-        pair2<ORDER, true>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
+        pair2<ORDER, true, CEN>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
+        pair2<ORDER, true, CEN>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
       }
     }
 #pragma unroll
