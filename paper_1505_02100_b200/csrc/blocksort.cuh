@@ -1,0 +1,85 @@
+// blocksort.cuh -- ascending sort of radix keys (bits2key of the float bits) for small and
+// medium n, shared by sort.cu (multi-kernel path) and fused.cu (single launch).
+//
+//  * warp_sort256: a warp sorts 256 keys held 8 per lane in registers (bitonic network;
+//    strides < 8 inside a lane, strides >= 8 across lanes by __shfl_xor_sync) -- no shared
+//    memory, no barriers;
+//  * cta_sort2048: 8 warps sort 8 runs of 256, then every key finds its final position by
+//    merging by rank: its index in its own run plus, for every other run, the number of keys
+//    below it (binary search in shared memory; keys of earlier runs that are equal count too,
+//    so ranks are unique).  Equal keys are identical bit patterns, so the output is THE
+//    ascending array (the same one the radix sort produces);
+//  * across CTAs (sort.cu): the same rank merge over sorted blocks of 2048 in global memory.
+#pragma once
+#include "common.cuh"
+
+namespace plg {
+
+constexpr int kBlockSortN = 2048;  // keys per CTA (256 threads x 8)
+
+// bitonic sort of the 256 keys k[0..7] of the 32 lanes (lane l holds positions 8l .. 8l+7)
+__device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int kk = 2; kk <= 256; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 8) {  // partner lane = lane ^ (j / 8), same register
+        const int lm = j >> 3;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const unsigned int o = __shfl_xor_sync(0xffffffffu, k[r], lm);
+          const bool asc = (((lane << 3) + r) & kk) == 0;
+          k[r] = (lower == asc) ? min(k[r], o) : max(k[r], o);
+        }
+      } else {  // inside the lane: registers r and r | j
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          if (r & j) continue;
+          const bool asc = (((lane << 3) + r) & kk) == 0;
+          const unsigned int a = k[r], b = k[r | j];
+          if ((a > b) == asc) { k[r] = b; k[r | j] = a; }
+        }
+      }
+    }
+  }
+}
+
+// first index in the sorted run a[0..len) with a[i] > v (upper) or a[i] >= v (lower)
+template <bool UPPER>
+__device__ __forceinline__ int run_bound(const unsigned int* a, int len, unsigned int v) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const unsigned int x = a[mid];
+    if (UPPER ? (x <= v) : (x < v)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff).  On
+// return out[0 .. 2048) holds the ascending array; runs (2048 words of shared memory) is
+// scratch.  Contains __syncthreads().
+__device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* runs, unsigned int* out) {
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  warp_sort256(k);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) runs[(w << 8) + (lane << 3) + r] = k[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const unsigned int v = k[r];
+    int rank = (lane << 3) + r;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) {
+      if (w2 < w) rank += run_bound<true>(runs + (w2 << 8), 256, v);
+      else if (w2 > w) rank += run_bound<false>(runs + (w2 << 8), 256, v);
+    }
+    out[rank] = v;
+  }
+  __syncthreads();
+}
+
+}  // namespace plg

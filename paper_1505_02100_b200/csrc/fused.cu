@@ -15,6 +15,7 @@
 // code as the multi-kernel path, so the result is bit-identical to it (tested).
 #include <cooperative_groups.h>
 
+#include "blocksort.cuh"
 #include "common.cuh"
 #include "psi_tile.cuh"
 #include "steps.cuh"
@@ -40,22 +41,6 @@ namespace plg {
   } while (0)
 #endif
 
-// ascending bitonic sort of npad (a power of two) keys in shared memory, whole CTA
-__device__ __forceinline__ void cta_bitonic_sort(unsigned int* key, int npad) {
-  for (int k = 2; k <= npad; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (npad >> 1); i += blockDim.x) {
-        const int lo = 2 * i - (i & (j - 1));  // lower index of the i-th pair at stride j
-        const int hi = lo + j;
-        const bool asc = (lo & k) == 0;
-        const unsigned int a = key[lo], b = key[hi];
-        if ((a > b) == asc) { key[lo] = b; key[hi] = a; }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 __device__ __forceinline__ Fx128 ldcg_fx(const Fx128* p) {
   Fx128 r;
   r.lo = __ldcg(&p->lo);
@@ -65,9 +50,8 @@ __device__ __forceinline__ Fx128 ldcg_fx(const Fx128* p) {
 
 template <int R>
 __global__ void __launch_bounds__(kPsiThreads)
-plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, int skip, plugin_result* out,
-                    Fx128* parts) {
-  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded
+plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, plugin_result* out, Fx128* parts) {
+  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded; then sort scratch
   __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
   __shared__ int sh_bad[8];
   __shared__ double p1[2 * 8];
@@ -79,11 +63,16 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int npad, int nsx, i
   const int tid = threadIdx.x;
 
   FT_MARK(0);
-  // sort (keys of the raw bits: pads are 0xffffffff and sort last)
-  for (int i = tid; i < npad; i += kPsiThreads)
-    key[i] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
-  __syncthreads();
-  cta_bitonic_sort(key, npad);
+  // sort (keys of the raw bits: pads are 0xffffffff and sort last): blocksort.cuh, n <= 2048
+  {
+    unsigned int k[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = 8 * tid + r;
+      k[r] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
+    }
+    cta_sort2048(k, key + nsx, key);  // runs: the 2048 words after the sample
+  }
   FT_MARK(1);
   for (int i = tid; i < n; i += kPsiThreads) key[i] = key2bits(key[i]);
   __syncthreads();
@@ -172,22 +161,20 @@ cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<0>, kPsiThreads,
-                                                  sizeof(float) * kFusedMaxN);
+                                                  sizeof(float) * 2 * kBlockSortN);
     max_grid = coop ? sms * occ : 0;
     if (max_grid > kFusedMaxGrid) max_grid = kFusedMaxGrid;
   }
   if (max_grid <= 0) return cudaErrorNotSupported;
-  int npad = 2;
-  while (npad < n) npad <<= 1;
   const int64_t T = kPsiSmallT, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
-  int nsx = (int)(nb * T > npad ? nb * T : npad);
+  int nsx = (int)(nb * T > kBlockSortN ? nb * T : kBlockSortN);  // cta_sort2048 writes 2048 positions
   // one CTA per SM at most: every CTA sorts its own copy of X, so more CTAs than SMs add no speed
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int grid = (int)(tiles < max_grid ? tiles : max_grid);
   if (grid > sms) grid = sms;
-  size_t smem = sizeof(float) * (size_t)nsx;
-  void* args[] = {(void*)&x, (void*)&n, (void*)&npad, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
+  size_t smem = sizeof(float) * ((size_t)nsx + kBlockSortN);  // sample + sort scratch
+  void* args[] = {(void*)&x, (void*)&n, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
   return cudaLaunchCooperativeKernel((const void*)plugin_fused_kernel<0>, dim3(grid), dim3(kPsiThreads), args, smem,
                                      s);
 }

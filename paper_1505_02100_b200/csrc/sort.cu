@@ -10,6 +10,7 @@
 // digit with 8 stable 1-bit splits in shared memory).
 #include <cstdlib>
 
+#include "blocksort.cuh"
 #include "common.cuh"
 
 namespace plg {
@@ -138,29 +139,55 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const void* 
   }
 }
 
-// n <= kSortSmallMax: the whole sort in one CTA of 1024 threads -- ascending bitonic sort of the
-// radix keys in shared memory (pads 0xffffffff sort last), the same unique ascending array as
-// the 4-pass radix sort in 1 launch instead of 12 (the launches dominate at these sizes).
-constexpr int kSortSmallMax = 16384;
-__global__ void __launch_bounds__(1024) sort_small_kernel(const float* __restrict__ x, int64_t n, int npad,
-                                                          float* __restrict__ xs) {
-  extern __shared__ unsigned int key[];
-  for (int i = threadIdx.x; i < npad; i += 1024)
-    key[i] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
-  __syncthreads();
-  for (int k = 2; k <= npad; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (npad >> 1); i += 1024) {
-        const int lo = 2 * i - (i & (j - 1));  // lower index of the i-th pair at stride j
-        const int hi = lo + j;
-        const bool asc = (lo & k) == 0;
-        const unsigned int a = key[lo], b = key[hi];
-        if ((a > b) == asc) { key[lo] = b; key[hi] = a; }
-      }
-      __syncthreads();
-    }
+// n <= kBlockSortMax: block sort + rank merge (blocksort.cuh) in 1-2 launches instead of the
+// 12 of the radix sort (launch-bound at these sizes); the same ascending array.
+constexpr int64_t kBlockSortMax = 262144;
+
+// block b of 2048 keys sorted in shared memory -> tmp (or straight to xs as floats when the
+// whole sample is one block)
+__global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict__ x, int64_t n,
+                                                         unsigned int* __restrict__ tmp, float* __restrict__ xs) {
+  __shared__ unsigned int runs[kBlockSortN];
+  __shared__ unsigned int out[kBlockSortN];
+  const int64_t base = (int64_t)blockIdx.x * kBlockSortN;
+  unsigned int k[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t i = base + 8 * threadIdx.x + r;
+    k[r] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
   }
-  for (int i = threadIdx.x; i < n; i += 1024) reinterpret_cast<unsigned int*>(xs)[i] = key2bits(key[i]);
+  cta_sort2048(k, runs, out);
+  const int cnt = (int)((n - base) < kBlockSortN ? (n - base) : kBlockSortN);
+  if (gridDim.x == 1) {
+    for (int i = threadIdx.x; i < cnt; i += 256) reinterpret_cast<unsigned int*>(xs)[i] = key2bits(out[i]);
+  } else {
+    for (int i = threadIdx.x; i < cnt; i += 256) tmp[base + i] = out[i];
+  }
+}
+
+// every key of the sorted blocks to its final position: its index in its block plus, per other
+// block, the keys below it (keys of earlier blocks that are equal count too: unique ranks)
+__global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __restrict__ tmp, int64_t n, int nblocks,
+                                                         float* __restrict__ xs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / kBlockSortN);
+    const unsigned int v = __ldg(tmp + i);
+    int64_t rank = i - (int64_t)b * kBlockSortN;
+    for (int b2 = 0; b2 < nblocks; ++b2) {
+      if (b2 == b) continue;
+      const unsigned int* run = tmp + (int64_t)b2 * kBlockSortN;
+      const int len = (int)((n - (int64_t)b2 * kBlockSortN) < kBlockSortN ? (n - (int64_t)b2 * kBlockSortN) : kBlockSortN);
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const unsigned int xv = __ldg(run + mid);
+        if (b2 < b ? (xv <= v) : (xv < v)) lo = mid + 1;
+        else hi = mid;
+      }
+      rank += lo;
+    }
+    reinterpret_cast<unsigned int*>(xs)[rank] = key2bits(v);
+  }
 }
 
 // x (float) -> xs (float, ascending).  tmp: n uint32; hist: 256*nb uint32.
@@ -172,16 +199,13 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
     const char* e = getenv("PLUGIN_SORT_RADIX");
     force_radix = (e && e[0] == '1') ? 1 : 0;
   }
-  if (n <= kSortSmallMax && !force_radix) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sort_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(unsigned int) * kSortSmallMax));
-      attr = true;
+  if (n <= kBlockSortMax && !force_radix) {
+    const int nblocks = (int)((n + kBlockSortN - 1) / kBlockSortN);
+    sort_block_kernel<<<nblocks, 256, 0, s>>>(x, n, tmp, xs);
+    if (nblocks > 1) {
+      const int64_t want = (n + 255) / 256;
+      sort_merge_kernel<<<(unsigned)(want < 4 * 148 ? want : 4 * 148), 256, 0, s>>>(tmp, n, nblocks, xs);
     }
-    int npad = 2;
-    while (npad < n) npad <<= 1;
-    sort_small_kernel<<<1, 1024, sizeof(unsigned int) * (size_t)npad, s>>>(x, n, npad, xs);
     return cudaGetLastError();
   }
   unsigned int* xk = reinterpret_cast<unsigned int*>(xs);

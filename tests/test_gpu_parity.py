@@ -309,14 +309,17 @@ def test_fused_toy_data_bit_identical(P):
     assert rel(a["h"], 0.96146759322923324) < TOL   # SURVEY App. B.2 (50-digit value)
 
 
-def test_small_sort_matches_radix_sort_bit_for_bit(P):
-    # n <= 16384 sorts in one CTA (bitonic on the radix keys); PLUGIN_SORT_RADIX=1 forces the
-    # 4-pass radix sort: both give the same unique ascending array, hence identical results
+@pytest.mark.parametrize("n", [2049, 12020, 131077, 262144])
+def test_small_sort_matches_radix_sort_bit_for_bit(P, n):
+    # n <= 262144 sorts by blocks of 2048 + a rank merge (blocksort.cuh); PLUGIN_SORT_RADIX=1
+    # forces the 4-pass radix sort: both give the same unique ascending array, hence identical
+    # results (ties, +-0 and tiny values included)
     import subprocess
     import sys
     code = ("import json, numpy as np, torch; from paper_1505_02100_b200 import plugin as P, inputs;"
-            "x = np.concatenate([inputs.mixture(9000, 12), np.array([0.0, -0.0, 1e-30, -1e-30] * 5, np.float32),"
-            " inputs.ties(3000, 1)]).astype(np.float32);"
+            f"n = {n};"
+            "x = np.concatenate([inputs.mixture(n - 20 - n // 4, 12), np.array([0.0, -0.0, 1e-30, -1e-30] * 5, np.float32),"
+            " inputs.ties(n // 4, 1)]).astype(np.float32);"
             "r = P.read_result(P.plugin_h(torch.from_numpy(x).cuda(), flags=P.PLUGIN_MULTI_KERNEL));"
             "print(json.dumps({k: float(v).hex() for k, v in r.items()}))")
     env = dict(__import__("os").environ)
