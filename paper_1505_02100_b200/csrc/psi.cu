@@ -82,16 +82,15 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
     if (jcount == T) {
       const float4* src = reinterpret_cast<const float4*>(xs + j0);
       float4* dst = reinterpret_cast<float4*>(sx);
-#pragma unroll
-      for (int q = 0; q < T / 4 / kPsiThreads; ++q) {
-        float4 v = __ldg(src + q * kPsiThreads + tid);
-        v.x = __fsub_rn(v.x, cen);
+      // T / 4 float4 per tile: one per thread for T >= 1024, the first T / 4 threads otherwise
+      for (int q = tid; q < T / 4; q += kPsiThreads) {
+        float4 v = __ldg(src + q);
+        v.x = __fsub_rn(v.x, cen);  // cen = 0 (exact no-op) for the small tiles of R = 0
         v.y = __fsub_rn(v.y, cen);
         v.z = __fsub_rn(v.z, cen);
         v.w = __fsub_rn(v.w, cen);
-        dst[q * kPsiThreads + tid] = v;
+        dst[q] = v;
       }
-      if (T / 4 < kPsiThreads && tid < T / 4) dst[tid] = __ldg(src + tid);  // R = 0 (cen = 0)
     } else {
       for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + j0 + q) : xpad, cen);
     }
