@@ -46,22 +46,10 @@ __device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
   }
 }
 
-// first index in the sorted run a[0..len) with a[i] > v (upper) or a[i] >= v (lower)
-template <bool UPPER>
-__device__ __forceinline__ int run_bound(const unsigned int* a, int len, unsigned int v) {
-  int lo = 0, hi = len;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const unsigned int x = a[mid];
-    if (UPPER ? (x <= v) : (x < v)) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff).  On
 // return out[0 .. 2048) holds the ascending array; runs (2048 words of shared memory) is
-// scratch.  Contains __syncthreads().
+// scratch.  The 7 searches of a key run in lockstep, branch-free (9 steps each: counts 0..256),
+// so their shared-memory loads overlap.  Contains __syncthreads().
 __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* runs, unsigned int* out) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   warp_sort256(k);
@@ -71,12 +59,24 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const unsigned int v = k[r];
+    int pos[8];
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) pos[w2] = 0;
+    // steps 256 .. 1: counts 0 .. 256 (positions past the run read as +inf)
+#pragma unroll
+    for (int step = 256; step > 0; step >>= 1) {
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) {
+        // runs before ours count keys <= v, runs after ours keys < v: unique ranks
+        const int idx = pos[w2] + step - 1;
+        const unsigned int x = idx < 256 ? runs[(w2 << 8) + idx] : 0xffffffffu;
+        const bool below = (w2 < w) ? (x <= v) : (x < v);
+        pos[w2] += below ? step : 0;
+      }
+    }
     int rank = (lane << 3) + r;
 #pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) {
-      if (w2 < w) rank += run_bound<true>(runs + (w2 << 8), 256, v);
-      else if (w2 > w) rank += run_bound<false>(runs + (w2 << 8), 256, v);
-    }
+    for (int w2 = 0; w2 < 8; ++w2) rank += (w2 == w) ? 0 : pos[w2];
     out[rank] = v;
   }
   __syncthreads();

@@ -309,9 +309,9 @@ def test_fused_toy_data_bit_identical(P):
     assert rel(a["h"], 0.96146759322923324) < TOL   # SURVEY App. B.2 (50-digit value)
 
 
-@pytest.mark.parametrize("n", [2049, 12020, 131077, 262144])
+@pytest.mark.parametrize("n", [2049, 4096, 12020, 30001, 32768])
 def test_small_sort_matches_radix_sort_bit_for_bit(P, n):
-    # n <= 262144 sorts by blocks of 2048 + a rank merge (blocksort.cuh); PLUGIN_SORT_RADIX=1
+    # n <= 32768 sorts by blocks of 2048 + a rank merge (blocksort.cuh); PLUGIN_SORT_RADIX=1
     # forces the 4-pass radix sort: both give the same unique ascending array, hence identical
     # results (ties, +-0 and tiny values included)
     import subprocess
