@@ -234,6 +234,13 @@ plugin_status kde_prepare(const float* d_x, int64_t n, void* d_ws, size_t ws_byt
 plugin_status kde_eval_prepared(int64_t n, double h, const float* d_points, int64_t m, double* d_f,
                                 void* d_ws, size_t ws_bytes, void* stream);
 
+/* The ordering step of the path (not a step of Alg. 1: it fixes the summation order, DESIGN.md
+ * §6.4): d_sorted (device float32[n]) = X in ascending order of the IEEE bits' total order
+ * (-NaN < -Inf < ... < -0 < +0 < ... < +Inf < +NaN), i.e. the unique array the passes read.
+ * Needs plugin_workspace_bytes(n); asynchronous. */
+plugin_status plugin_sort(const float* d_x, int64_t n, float* d_sorted, void* d_ws, size_t ws_bytes,
+                          void* stream);
+
 /* Text of the last non-OK return on this thread ("" if none).  Static storage. */
 const char* plugin_last_error(void);
 

@@ -265,6 +265,21 @@ plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_ou
   return after(1, d_total, d_out, stream);
 }
 
+plugin_status plugin_sort(const float* d_x, int64_t n, float* d_sorted, void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_x || !d_sorted) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sort");
+  if ((e = cudaMemcpyAsync(d_sorted, w.xs, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "copy sorted");
+  return PLUGIN_OK;
+}
+
 plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_result* d_out, void* d_ws,
                          size_t ws_bytes, void* stream) {
   g_err[0] = 0;

@@ -83,6 +83,7 @@ def lib():
             "plugin_num_tiles": (i64, [i64]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
+            "plugin_sort": (i32, [P, i64, P, P, sz, P]),
             "plugin_q32_workspace_bytes": (sz, [i64]),
             "psi_r_q32": (i32, [P, i64, i64, i32, P, P, sz, P]),
             "plugin_h_q32": (i32, [P, i64, P, P, sz, P]),
@@ -106,7 +107,7 @@ PLUGIN_MULTI_KERNEL = 2
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_dpi", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
+            "plugin_shard_tiles", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
             "kde_workspace_bytes", "kde_eval", "kde_prepare",
             "kde_eval_prepared", "plugin_last_error", "plugin_version")
 
@@ -325,6 +326,16 @@ def kde_eval_prepared(n: int, h: float, points: torch.Tensor, ws: torch.Tensor, 
     out = torch.empty(m, dtype=torch.float64, device=points.device) if out is None else out
     _check(lib().kde_eval_prepared(int(n), float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(), ws.numel(),
                                    _stream(stream)))
+    return out
+
+
+def plugin_sort(x: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """The sorted copy of X the passes read (device float32, asynchronous)."""
+    x = _x(x)
+    n = x.numel()
+    ws = workspace(n, x.device) if ws is None else ws
+    out = torch.empty_like(x)
+    _check(lib().plugin_sort(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
 
 

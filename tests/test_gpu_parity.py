@@ -359,3 +359,25 @@ def test_plain_c_example_uses_the_abi(P, tmp_path):
     g = _golden(1)
     for k in ("psi6", "psi4", "h"):
         assert rel(r[k], g[k]) < TOL
+
+
+def _key_sorted(x):
+    # ascending order of the IEEE-754 bits' total order (the radix key of sort.cu), numpy only
+    b = x.astype(np.float32).view(np.uint32)
+    key = np.where(b & 0x80000000, ~b, b | 0x80000000).astype(np.uint32)
+    return x.astype(np.float32)[np.argsort(key, kind="stable")]
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 255, 256, 257, 1000, 2047, 2048, 2049, 4095, 4097, 12020, 30001, 32768,
+                               32769, 100003])
+def test_sort_is_exact(P, n):
+    # the block sort (n <= 32768) and the radix sort (above) against numpy, bit for bit:
+    # ties, +-0, denormals and the extremes of every run included
+    rng = np.random.default_rng(n)
+    x = rng.normal(0, 1, n).astype(np.float32)
+    x[::7] = np.round(x[::7], 1)                      # ties
+    if n > 8:
+        x[:4] = [0.0, -0.0, 1e-40, -1e-40]
+        x[-3:] = [3e38, -3e38, 0.5]
+    got = P.plugin_sort(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), _key_sorted(x).view(np.uint32))
