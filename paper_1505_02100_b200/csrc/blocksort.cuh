@@ -62,15 +62,16 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
     int pos[8];
 #pragma unroll
     for (int w2 = 0; w2 < 8; ++w2) pos[w2] = 0;
-    // steps 256 .. 1: counts 0 .. 256 (positions past the run read as +inf)
+    // steps 256 .. 1: counts 0 .. 256 (positions past the run never count)
 #pragma unroll
     for (int step = 256; step > 0; step >>= 1) {
 #pragma unroll
       for (int w2 = 0; w2 < 8; ++w2) {
         // runs before ours count keys <= v, runs after ours keys < v: unique ranks
         const int idx = pos[w2] + step - 1;
-        const unsigned int x = idx < 256 ? runs[(w2 << 8) + idx] : 0xffffffffu;
-        const bool below = (w2 < w) ? (x <= v) : (x < v);
+        const bool in = idx < 256;
+        const unsigned int x = runs[(w2 << 8) + (in ? idx : 255)];
+        const bool below = in && ((w2 < w) ? (x <= v) : (x < v));  // past the run: never below
         pos[w2] += below ? step : 0;
       }
     }

@@ -184,9 +184,10 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
           const int b2 = b0 + q;
           const int off = pos[q] + step - 1;
           const int64_t idx = (int64_t)b2 * kBlockSortN + off;
-          // positions past a block, the sample or the block count act as +inf
-          const unsigned int x = (b2 < nblocks && off < kBlockSortN && idx < n) ? __ldg(tmp + idx) : 0xffffffffu;
-          const bool below = (b2 < b) ? (x <= v) : (x < v);
+          // positions past a block, the sample or the block count never count
+          const bool in = b2 < nblocks && off < kBlockSortN && idx < n;
+          const unsigned int x = in ? __ldg(tmp + idx) : 0u;
+          const bool below = in && ((b2 < b) ? (x <= v) : (x < v));
           pos[q] += below ? step : 0;
         }
       }
