@@ -3,13 +3,15 @@
 //
 //  * warp_sort256: a warp sorts 256 keys held 8 per lane in registers (bitonic network;
 //    strides < 8 inside a lane, strides >= 8 across lanes by __shfl_xor_sync) -- no shared
-//    memory, no barriers;
+//    memory, no barriers, no branches;
 //  * cta_sort2048: 8 warps sort 8 runs of 256, then every key finds its final position by
 //    merging by rank: its index in its own run plus, for every other run, the number of keys
-//    below it (binary search in shared memory; keys of earlier runs that are equal count too,
-//    so ranks are unique).  Equal keys are identical bit patterns, so the output is THE
-//    ascending array (the same one the radix sort produces);
+//    below it (branch-free binary searches in shared memory; keys of earlier runs that are equal
+//    count too, so ranks are unique).  Equal keys are identical bit patterns, so the output is
+//    THE ascending array (the same one the radix sort produces);
 //  * across CTAs (sort.cu): the same rank merge over sorted blocks of 2048 in global memory.
+// The routines run once per launch, so the stage loops stay rolled: fully unrolled they are
+// ~10k instructions fetched cold from L2 (measured 26 us for 2048 keys).
 #pragma once
 #include "common.cuh"
 
@@ -17,32 +19,41 @@ namespace plg {
 
 constexpr int kBlockSortN = 2048;  // keys per CTA (256 threads x 8)
 
+__device__ __forceinline__ void cmpx(unsigned int& a, unsigned int& b, bool asc) {
+  const unsigned int lo = min(a, b), hi = max(a, b);
+  a = asc ? lo : hi;
+  b = asc ? hi : lo;
+}
+
 // bitonic sort of the 256 keys k[0..7] of the 32 lanes (lane l holds positions 8l .. 8l+7)
 __device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
+#pragma unroll 1
   for (int kk = 2; kk <= 256; kk <<= 1) {
+    // strides >= 8: partner lane = lane ^ (j / 8), same register
+#pragma unroll 1
+    for (int j = kk >> 1; j >= 8; j >>= 1) {
+      const int lm = j >> 3;
+      const bool lower = (lane & lm) == 0;
+      const bool asc = ((lane << 3) & kk) == 0;  // kk >= 16: bit kk of 8 lane + r does not depend on r
 #pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= 8) {  // partner lane = lane ^ (j / 8), same register
-        const int lm = j >> 3;
-        const bool lower = (lane & lm) == 0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const unsigned int o = __shfl_xor_sync(0xffffffffu, k[r], lm);
-          const bool asc = (((lane << 3) + r) & kk) == 0;
-          k[r] = (lower == asc) ? min(k[r], o) : max(k[r], o);
-        }
-      } else {  // inside the lane: registers r and r | j
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          if (r & j) continue;
-          const bool asc = (((lane << 3) + r) & kk) == 0;
-          const unsigned int a = k[r], b = k[r | j];
-          if ((a > b) == asc) { k[r] = b; k[r | j] = a; }
-        }
+      for (int r = 0; r < 8; ++r) {
+        const unsigned int o = __shfl_xor_sync(0xffffffffu, k[r], lm);
+        k[r] = (lower == asc) ? min(k[r], o) : max(k[r], o);
       }
     }
+    // strides 4, 2, 1 inside the lane (kk = 2, 4 start lower)
+    if (kk >= 8) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cmpx(k[r], k[r + 4], (((lane << 3) + r) & kk) == 0);
+    }
+    if (kk >= 4) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (!(r & 2)) cmpx(k[r], k[r + 2], (((lane << 3) + r) & kk) == 0);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r += 2) cmpx(k[r], k[r + 1], (((lane << 3) + r) & kk) == 0);
   }
 }
 
@@ -56,9 +67,10 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
 #pragma unroll
   for (int r = 0; r < 8; ++r) runs[(w << 8) + (lane << 3) + r] = k[r];
   __syncthreads();
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < 8; ++r) {
-    const unsigned int v = k[r];
+    const int mine = (lane << 3) + r;
+    const unsigned int v = runs[(w << 8) + mine];
     int pos[8];
 #pragma unroll
     for (int w2 = 0; w2 < 8; ++w2) pos[w2] = 0;
@@ -75,7 +87,7 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
         pos[w2] += below ? step : 0;
       }
     }
-    int rank = (lane << 3) + r;
+    int rank = mine;
 #pragma unroll
     for (int w2 = 0; w2 < 8; ++w2) rank += (w2 == w) ? 0 : pos[w2];
     out[rank] = v;
