@@ -4,14 +4,13 @@
 //  * warp_sort256: a warp sorts 256 keys held 8 per lane in registers (bitonic network;
 //    strides < 8 inside a lane, strides >= 8 across lanes by __shfl_xor_sync) -- no shared
 //    memory, no barriers, no branches;
-//  * cta_sort2048: 8 warps sort 8 runs of 256, then every key finds its final position by
-//    merging by rank: its index in its own run plus, for every other run, the number of keys
-//    below it (branch-free binary searches in shared memory; keys of earlier runs that are equal
-//    count too, so ranks are unique).  Equal keys are identical bit patterns, so the output is
-//    THE ascending array (the same one the radix sort produces);
-//  * across CTAs (sort.cu): the same rank merge over sorted blocks of 2048 in global memory.
-// The routines run once per launch, so the stage loops stay rolled: fully unrolled they are
-// ~10k instructions fetched cold from L2 (measured 26 us for 2048 keys).
+//  * cta_sort2048: 8 warps sort 8 runs of 256, then 3 rounds of pairwise merges by rank
+//    (branch-free binary searches in shared memory; a partner run that comes first counts
+//    equal keys too, so positions are unique).  Equal keys are identical bit patterns, so the
+//    output is THE ascending array (the same one the radix sort produces);
+//  * across CTAs (sort.cu): a rank merge over sorted blocks of 2048 in global memory.
+// The routines run once per launch, so the loops stay rolled: fully unrolled they were ~10k
+// instructions fetched cold from L2 (measured 26 us for 2048 keys).
 #pragma once
 #include "common.cuh"
 
@@ -57,42 +56,54 @@ __device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
   }
 }
 
-// 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff).  On
-// return out[0 .. 2048) holds the ascending array; runs (2048 words of shared memory) is
-// scratch.  The 7 searches of a key run in lockstep, branch-free (9 steps each: counts 0..256),
-// so their shared-memory loads overlap.  Contains __syncthreads().
-__device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* runs, unsigned int* out) {
+// 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff, real keys
+// <= 0xfffffffe -- see blocksort_key).  On return out[0 .. 2048) holds the ascending array; a
+// (2048 words of shared memory) is scratch.  After the warp sorts, three rounds of pairwise
+// merges by rank (runs of 256 -> 512 -> 1024 -> 2048): a key's position in the merged run is its
+// index in its run plus the keys of the partner run below it (an earlier partner counts equal
+// keys too, so positions are unique): one branch-free binary search per key per round.
+// Contains __syncthreads().
+__device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* a, unsigned int* out) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   warp_sort256(k);
 #pragma unroll
-  for (int r = 0; r < 8; ++r) runs[(w << 8) + (lane << 3) + r] = k[r];
+  for (int r = 0; r < 8; ++r) a[(w << 8) + (lane << 3) + r] = k[r];
   __syncthreads();
+  unsigned int* src = a;
+  unsigned int* dst = out;
 #pragma unroll 1
-  for (int r = 0; r < 8; ++r) {
-    const int mine = (lane << 3) + r;
-    const unsigned int v = runs[(w << 8) + mine];
-    int pos[8];
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) pos[w2] = 0;
-    // steps 256 .. 1: counts 0 .. 256 (positions past the run never count)
-#pragma unroll
-    for (int step = 256; step > 0; step >>= 1) {
-#pragma unroll
-      for (int w2 = 0; w2 < 8; ++w2) {
-        // runs before ours count keys <= v, runs after ours keys < v: unique ranks
-        const int idx = pos[w2] + step - 1;
-        const bool in = idx < 256;
-        const unsigned int x = runs[(w2 << 8) + (in ? idx : 255)];
-        const bool below = in && ((w2 < w) ? (x <= v) : (x < v));  // past the run: never below
-        pos[w2] += below ? step : 0;
+  for (int lg = 8; lg < 11; ++lg) {  // run length L = 2^lg
+    const int L = 1 << lg;
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r) {
+      const int p = (tid << 3) + r;
+      const unsigned int v = src[p];
+      const int run = p >> lg, i = p & (L - 1);
+      const bool later = run & 1;  // the partner run comes first
+      const unsigned int* part = src + ((run ^ 1) << lg);
+      const unsigned int t = later ? v + 1u : v;  // count keys < t; v + 1 wraps only for pads
+      int pos = 0;
+#pragma unroll 1
+      for (int step = L; step > 0; step >>= 1) {  // counts 0 .. L
+        const int idx = pos + step - 1;
+        const unsigned int x = part[idx < L ? idx : L - 1];
+        pos += (idx < L && x < t) ? step : 0;
       }
+      if (later && v == 0xffffffffu) pos = L;  // a pad after the partner run: all of it comes first
+      dst[((run & ~1) << lg) + i + pos] = v;
     }
-    int rank = mine;
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) rank += (w2 == w) ? 0 : pos[w2];
-    out[rank] = v;
+    __syncthreads();
+    unsigned int* tmp = src;
+    src = dst;
+    dst = tmp;
   }
-  __syncthreads();
+  // three rounds: the result is in out (src after the last swap)
+}
+
+// the sort key of a float's bits, with the NaN 0x7fffffff folded onto 0x7ffffffe (another NaN)
+// so that 0xffffffff marks only the pads of cta_sort2048
+__device__ __forceinline__ unsigned int blocksort_key(unsigned int bits) {
+  return min(bits2key(bits), 0xfffffffeu);
 }
 
 }  // namespace plg

@@ -69,7 +69,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int i = 8 * tid + r;
-      k[r] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
+      k[r] = (i < n) ? blocksort_key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
     }
     cta_sort2048(k, key + nsx, key);  // runs: the 2048 words after the sample
   }

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int64_t i = base + 8 * threadIdx.x + r;
-    k[r] = (i < n) ? bits2key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
+    k[r] = (i < n) ? blocksort_key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
   }
   cta_sort2048(k, runs, out);
   const int cnt = (int)((n - base) < kBlockSortN ? (n - base) : kBlockSortN);
@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
           // positions past a block, the sample or the block count never count
           const bool in = b2 < nblocks && off < kBlockSortN && idx < n;
           const unsigned int x = in ? __ldg(tmp + idx) : 0u;
-          const bool below = in && ((b2 < b) ? (x <= v) : (x < v));
-          pos[q] += below ? step : 0;
+          // earlier blocks count equal keys too: x < v + 1 (real keys are <= 0xfffffffe)
+          pos[q] += (in && x < ((b2 < b) ? v + 1u : v)) ? step : 0;
         }
       }
 #pragma unroll
