@@ -169,30 +169,29 @@ __global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict
 // block, the keys below it (keys of earlier blocks that are equal count too: unique ranks)
 __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __restrict__ tmp, int64_t n, int nblocks,
                                                          float* __restrict__ xs) {
+  // all sorted blocks in shared memory (n <= kBlockSortMax: <= 128 KB), then shared-memory searches
+  extern __shared__ unsigned int sb[];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sb[i] = __ldg(tmp + i);
+  __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / kBlockSortN);
-    const unsigned int v = __ldg(tmp + i);
+    const unsigned int v = sb[i];
     int64_t rank = i - (int64_t)b * kBlockSortN;
-    // branch-free 12-step searches (counts 0 .. 2048), four blocks in lockstep (independent
-    // loads in flight)
-    for (int b0 = 0; b0 < nblocks; b0 += 4) {
-      int pos[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int b2 = 0; b2 < nblocks; ++b2) {
+      if (b2 == b) continue;
+      const unsigned int* run = sb + (int64_t)b2 * kBlockSortN;
+      const int len = (int)((n - (int64_t)b2 * kBlockSortN) < kBlockSortN ? (n - (int64_t)b2 * kBlockSortN) : kBlockSortN);
+      // earlier blocks count equal keys too: x < v + 1 (real keys are <= 0xfffffffe)
+      const unsigned int t = (b2 < b) ? v + 1u : v;
+      int pos = 0;
 #pragma unroll
-      for (int step = kBlockSortN; step > 0; step >>= 1) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int b2 = b0 + q;
-          const int off = pos[q] + step - 1;
-          const int64_t idx = (int64_t)b2 * kBlockSortN + off;
-          // positions past a block, the sample or the block count never count
-          const bool in = b2 < nblocks && off < kBlockSortN && idx < n;
-          const unsigned int x = in ? __ldg(tmp + idx) : 0u;
-          // earlier blocks count equal keys too: x < v + 1 (real keys are <= 0xfffffffe)
-          pos[q] += (in && x < ((b2 < b) ? v + 1u : v)) ? step : 0;
-        }
+      for (int step = kBlockSortN; step > 0; step >>= 1) {  // counts 0 .. len, branch-free
+        const int idx = pos + step - 1;
+        const unsigned int x = run[idx < len ? idx : len - 1];
+        pos += (idx < len && x < t) ? step : 0;
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) rank += (b0 + q == b || b0 + q >= nblocks) ? 0 : pos[q];
+      rank += pos;
     }
     reinterpret_cast<unsigned int*>(xs)[rank] = key2bits(v);
   }
@@ -211,8 +210,15 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
     const int nblocks = (int)((n + kBlockSortN - 1) / kBlockSortN);
     sort_block_kernel<<<nblocks, 256, 0, s>>>(x, n, tmp, xs);
     if (nblocks > 1) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(sort_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(unsigned int) * kBlockSortMax));
+        attr = true;
+      }
       const int64_t want = (n + 255) / 256;
-      sort_merge_kernel<<<(unsigned)(want < 4 * 148 ? want : 4 * 148), 256, 0, s>>>(tmp, n, nblocks, xs);
+      sort_merge_kernel<<<(unsigned)(want < 148 ? want : 148), 256, sizeof(unsigned int) * (size_t)n, s>>>(
+          tmp, n, nblocks, xs);
     }
     return cudaGetLastError();
   }
