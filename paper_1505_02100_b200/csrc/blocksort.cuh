@@ -74,23 +74,34 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
 #pragma unroll 1
   for (int lg = 8; lg < 11; ++lg) {  // run length L = 2^lg
     const int L = 1 << lg;
-#pragma unroll 1
+    // the thread's 8 keys search in lockstep: 8 independent shared-memory loads per step
+    unsigned int v[8], t[8];
+    int pos[8], base[8];
+#pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int p = (tid << 3) + r;
-      const unsigned int v = src[p];
-      const int run = p >> lg, i = p & (L - 1);
-      const bool later = run & 1;  // the partner run comes first
-      const unsigned int* part = src + ((run ^ 1) << lg);
-      const unsigned int t = later ? v + 1u : v;  // count keys < t; v + 1 wraps only for pads
-      int pos = 0;
+      v[r] = src[p];
+      const int run = p >> lg;
+      const bool later = run & 1;                 // the partner run comes first
+      t[r] = later ? v[r] + 1u : v[r];            // count keys < t; v + 1 wraps only for pads
+      base[r] = (run ^ 1) << lg;
+      pos[r] = 0;
+    }
 #pragma unroll 1
-      for (int step = L; step > 0; step >>= 1) {  // counts 0 .. L
-        const int idx = pos + step - 1;
-        const unsigned int x = part[idx < L ? idx : L - 1];
-        pos += (idx < L && x < t) ? step : 0;
+    for (int step = L; step > 0; step >>= 1) {  // counts 0 .. L
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int idx = pos[r] + step - 1;
+        const unsigned int x = src[base[r] + (idx < L ? idx : L - 1)];
+        pos[r] += (idx < L && x < t[r]) ? step : 0;
       }
-      if (later && v == 0xffffffffu) pos = L;  // a pad after the partner run: all of it comes first
-      dst[((run & ~1) << lg) + i + pos] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = (tid << 3) + r;
+      const int run = p >> lg, i = p & (L - 1);
+      const int ps = ((run & 1) && v[r] == 0xffffffffu) ? L : pos[r];  // a pad after the partner run
+      dst[((run & ~1) << lg) + i + ps] = v[r];
     }
     __syncthreads();
     unsigned int* tmp = src;
