@@ -177,21 +177,32 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
     const int b = (int)(i / kBlockSortN);
     const unsigned int v = sb[i];
     int64_t rank = i - (int64_t)b * kBlockSortN;
+    // four blocks searched in lockstep (independent shared-memory loads per step)
 #pragma unroll 1
-    for (int b2 = 0; b2 < nblocks; ++b2) {
-      if (b2 == b) continue;
-      const unsigned int* run = sb + (int64_t)b2 * kBlockSortN;
-      const int len = (int)((n - (int64_t)b2 * kBlockSortN) < kBlockSortN ? (n - (int64_t)b2 * kBlockSortN) : kBlockSortN);
-      // earlier blocks count equal keys too: x < v + 1 (real keys are <= 0xfffffffe)
-      const unsigned int t = (b2 < b) ? v + 1u : v;
-      int pos = 0;
+    for (int b0 = 0; b0 < nblocks; b0 += 4) {
+      int pos[4], len[4], base[4];
+      unsigned int t[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int b2 = b0 + q;
+        const int64_t rem = n - (int64_t)b2 * kBlockSortN;
+        // missing blocks and our own count nothing (len 0); earlier blocks count equal keys too:
+        // x < v + 1 (real keys are <= 0xfffffffe)
+        len[q] = (b2 < nblocks && b2 != b) ? (int)(rem < kBlockSortN ? rem : kBlockSortN) : 0;
+        base[q] = b2 < nblocks ? b2 * kBlockSortN : 0;
+        t[q] = (b2 < b) ? v + 1u : v;
+        pos[q] = 0;
+      }
 #pragma unroll
       for (int step = kBlockSortN; step > 0; step >>= 1) {  // counts 0 .. len, branch-free
-        const int idx = pos + step - 1;
-        const unsigned int x = run[idx < len ? idx : len - 1];
-        pos += (idx < len && x < t) ? step : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int idx = pos[q] + step - 1;
+          const unsigned int x = sb[base[q] + (idx < len[q] ? idx : 0)];
+          pos[q] += (idx < len[q] && x < t[q]) ? step : 0;
+        }
       }
-      rank += pos;
+      rank += pos[0] + pos[1] + pos[2] + pos[3];
     }
     reinterpret_cast<unsigned int*>(xs)[rank] = key2bits(v);
   }
