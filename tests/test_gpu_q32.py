@@ -1,7 +1,9 @@
 """GPU parity of the Q32.32 datapath against the oracle:
 bit-exact integer totals for the pair sums (integer work: bit-exact is the bar), and h of the
 whole algorithm within the paper's fixed-point accuracy (Table 4, 4.2e-6 relative)."""
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -66,3 +68,32 @@ def test_q32_errors(P):
         P.psi_r_q32(zq, ONE, 5)
     r = P.read_result(P.plugin_h_q32(torch.full((100,), 1.5, device="cuda")))
     assert r["status"] == P.PLUGIN_E_DEGENERATE and math.isnan(r["h"])
+
+
+TABLE4 = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dump_table4():
+    # a Table 4-style accuracy table on the synthetic stand-in data, written next to
+    # the GPU evidence when gpurun_out/ exists
+    yield
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if TABLE4 and os.path.isdir(out):
+        with open(os.path.join(out, "table4.json"), "w") as f:
+            json.dump(TABLE4, f, indent=1, sort_keys=True)
+
+
+@pytest.mark.parametrize("n", list(range(128, 1025, 128)))
+def test_table4_accuracy_at_the_papers_sizes(P, oracle_mod, n):
+    # Table 4 reports |h - h_ref| / h_ref of the FPGA's Q32.32 designs against an fp64 C++ h_ref,
+    # at most 4.2e-6.  Here: the fp32 GPU path and the Q32.32 GPU path against the fp64
+    # oracle on N(0,1) samples of the paper's sizes (seeds 100..107)
+    x = inputs.normal(n, 100 + n // 128 - 1)
+    ref = oracle_mod.plugin(x)["h"]
+    xt = torch.from_numpy(x).cuda()
+    h32 = P.read_result(P.plugin_h(xt))["h"]
+    hq = P.read_result(P.plugin_h_q32(xt))["h"]
+    TABLE4[n] = {"h_ref": ref, "fp32_path": h32, "q32_path": hq, "rel_fp32": abs(h32 - ref) / ref,
+                 "rel_q32": abs(hq - ref) / ref}
+    assert TABLE4[n]["rel_fp32"] <= 4.2e-6 and TABLE4[n]["rel_q32"] <= 4.2e-6
