@@ -8,11 +8,12 @@
 // atomic counter.  Each thread keeps R rows i in registers and streams the tile's j values
 // from shared memory (one LDS.128 broadcast per 4 j); two pairs go through each packed
 // f32x2 instruction:
-//     d = x_j - x_i (difference first, raw fp32)   u = d*s (s = fp32(1/g))   t = u*u
-//     a = t*c + p_i   (c = fp32(-log2(e)/2), p_i in (-2, -1] a per-row phase)   e = ex2.approx(a)
-//     P6 = ((t - 15) t + 45) t - 15   |   P4 = (t - 6) t + 3      (exact integer coefficients)
+//     u = fma(x'_j, s_i, -x'_i s_i)   (x' = x - c, c the tile's first row; s = fp32(1/g))
+//     t = u*u   a = t*c + p_i   (c = fp32(-log2(e)/2), p_i in (-2, -1] a per-row phase)
+//     e = ex2.approx(a)   P6 = ((t - 15) t + 45) t - 15  |  P4 = (t - 6) t + 3  (exact integers)
 //     acc += P * e
-// i.e. 8 (r=6) / 7 (r=4) FP32 lane-ops and 1 MUFU.EX2 per pair.  Numerics:
+// i.e. 7 (r=6) / 6 (r=4) FP32 lane-ops and 1 MUFU.EX2 per pair (the small tiles of n <= 2048
+// use difference first, one op more).  Numerics:
 // the per-row phase p_i = -1 - frac(i * 0.618...) (24 random bits, a Weyl sequence)
 // dithers the SFU exp argument so the table-pattern bias of MUFU.EX2 averages to a
 // constant, and keeps |a| >= 1 (no input truncation inside MUFU); it is undone by scaling
