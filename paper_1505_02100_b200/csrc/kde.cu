@@ -61,6 +61,30 @@ __device__ __forceinline__ void kde_term2_poly(u64 xj, u64 p, u64 k2, u64& acc) 
   acc = add2(acc, ex2_fma2(pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f))));
 }
 
+// Centred form: with c a point of the block, the sample is staged as
+// x' = fl(X - c) and each point keeps -P = -fl(fl(x_k - c) sk), sk = fp32(sqrt(log2(e)/2)/h):
+// u = fma(x', sk, -P) = (X - x_k) sk, t = u^2, e = 2^-t (MUFU.EX2 takes the negation for free):
+// 3 FP32 lane-ops per term instead of 4.  Used when the block's points span <= 2.5 / sk (the
+// rounding of P is then <= 2.5 eps absolute in u); otherwise the difference-first terms above.
+__device__ __forceinline__ void kde_term2_c(u64 xj, u64 nP, u64 sk2, u64& acc) {
+  float t0, t1;
+  const u64 u = fma2(xj, sk2, nP);
+  upk2(mul2(u, u), t0, t1);
+  acc = add2(acc, pk2(ex2(-t0), ex2(-t1)));
+}
+__device__ __forceinline__ void kde_term2_c_poly(u64 xj, u64 nP, u64 sk2, u64& acc) {
+  float t0, t1;
+  const u64 u = fma2(xj, sk2, nP);
+  upk2(mul2(u, u), t0, t1);
+  acc = add2(acc, ex2_fma2(pk2(fmaxf(-t0, -126.f), fmaxf(-t1, -126.f))));
+}
+__device__ __forceinline__ void kde_term2_c_masked(u64 xj, u64 nP, u64 sk2, u64& acc, bool m0, bool m1) {
+  float t0, t1;
+  const u64 u = fma2(xj, sk2, nP);
+  upk2(mul2(u, u), t0, t1);
+  acc = add2(acc, pk2(m0 ? ex2(-t0) : 0.f, m1 ? ex2(-t1) : 0.f));
+}
+
 // first index i in [0, n) with xs[i] >= v (strict = false) or xs[i] > v (strict = true)
 __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
   int64_t lo = 0, hi = n;
@@ -73,6 +97,85 @@ __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
   return lo;
 }
 
+// the sample range [jb, je) against this thread's kKdeRG points (per-point fp64 sums in drow)
+template <bool HYB, bool CEN>
+__device__ __forceinline__ void kde_tiles(const float* __restrict__ xs, int64_t jb, int64_t je, float c,
+                                          const u64 (&p2)[kKdeRG], const u64 (&nP2)[kKdeRG], u64 k2, u64 sk2,
+                                          float* sx, double (&drow)[kKdeRG]) {
+  const int tid = threadIdx.x;
+  const float4* sx4 = reinterpret_cast<const float4*>(sx);
+  for (int64_t t0 = jb; t0 < je; t0 += kKdeTX) {
+    const int cnt = (int)((je - t0) < kKdeTX ? (je - t0) : kKdeTX);
+    __syncthreads();  // previous tile fully consumed
+    for (int q = tid; q < kKdeTX; q += kKdeThreads)
+      sx[q] = (q < cnt) ? (CEN ? __fsub_rn(__ldg(xs + t0 + q), c) : __ldg(xs + t0 + q)) : 0.f;
+    __syncthreads();
+    const int full = cnt / kKdeCH;
+    for (int c = 0; c < full; ++c) {
+      u64 acc[kKdeRG];
+#pragma unroll
+      for (int k = 0; k < kKdeRG; ++k) acc[k] = 0ull;
+#pragma unroll
+      for (int q = 0; q < kKdeCH / 4; ++q) {
+        const float4 v = sx4[c * (kKdeCH / 4) + q];
+        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+        for (int k = 0; k < kKdeRG; ++k) {
+          if (CEN) {
+            // hybrid: 5 term pairs in 16 take their exp on the FMA pipe (the LP optimum for
+            // 3 + 8 FP32 ops)
+            kde_term2_c(j01, nP2[k], sk2, acc[k]);
+            if (HYB && k < 2 + (q & 1)) kde_term2_c_poly(j23, nP2[k], sk2, acc[k]);
+            else kde_term2_c(j23, nP2[k], sk2, acc[k]);
+          } else {
+            kde_term2(j01, p2[k], k2, acc[k]);
+            // hybrid: one term pair in four takes its exp on the FMA pipe (kHybFrac = 1/4)
+            if (HYB && (q & 1)) kde_term2_poly(j23, p2[k], k2, acc[k]);
+            else kde_term2(j23, p2[k], k2, acc[k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kKdeRG; ++k) {
+        float a0, a1;
+        upk2(acc[k], a0, a1);
+        drow[k] += f32_to_f64_alu(a0 + a1);
+      }
+    }
+    if (full * kKdeCH < cnt) {  // ragged last chunk
+      u64 acc[kKdeRG];
+#pragma unroll
+      for (int k = 0; k < kKdeRG; ++k) acc[k] = 0ull;
+      for (int q = 0; q < kKdeCH / 4; ++q) {
+        const float4 v = sx4[full * (kKdeCH / 4) + q];
+        const int j = full * kKdeCH + 4 * q;
+        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
+#pragma unroll
+        for (int k = 0; k < kKdeRG; ++k) {
+          if (CEN) {
+            kde_term2_c_masked(j01, nP2[k], sk2, acc[k], j < cnt, j + 1 < cnt);
+            kde_term2_c_masked(j23, nP2[k], sk2, acc[k], j + 2 < cnt, j + 3 < cnt);
+          } else {
+            kde_term2_masked(j01, p2[k], k2, acc[k], j < cnt, j + 1 < cnt);
+            kde_term2_masked(j23, p2[k], k2, acc[k], j + 2 < cnt, j + 3 < cnt);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kKdeRG; ++k) {
+        float a0, a1;
+        upk2(acc[k], a0, a1);
+        drow[k] += f32_to_f64_alu(a0 + a1);
+      }
+    }
+  }
+
+}
+
+#ifndef KDE_CENTER
+#define KDE_CENTER 1  // 0: difference-first terms everywhere (A/B builds)
+#endif
+
 // resident CTAs per SM the register budget is sized for (tuning: -DKDE_OCC=3 fits 78 registers)
 #ifndef KDE_OCC
 #define KDE_OCC 2
@@ -80,12 +183,14 @@ __device__ int64_t bound(const float* xs, int64_t n, double v, bool strict) {
 
 template <bool HYB>
 __global__ void __launch_bounds__(kKdeThreads, KDE_OCC)
-kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pts, int64_t m, float kf, double cut,
+kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pts, int64_t m, float kf, float sk,
+           double cut,
            int S, double scale, const Ctrl* ctrl, double* __restrict__ partial, unsigned int* __restrict__ counters,
            double* __restrict__ f) {
   __shared__ __align__(16) float sx[kKdeTX];
   __shared__ float s_min[kKdeThreads / 32], s_max[kKdeThreads / 32];
   __shared__ long long s_lo, s_hi;
+  __shared__ float s_bmin, s_bmax;
   __shared__ int s_last;
   const int tid = threadIdx.x;
   const int64_t b = blockIdx.x / S;
@@ -116,67 +221,27 @@ kde_kernel(const float* __restrict__ xs, int64_t n, const float* __restrict__ pt
     for (int w = 0; w < kKdeThreads / 32; ++w) v = (tid == 0) ? fminf(v, s_min[w]) : fmaxf(v, s_max[w]);
     // samples outside [min - C, max + C] give exactly zero fp32 terms for every point of the block
     // (no non-NaN point: min = +inf, max = -inf, and the range below is empty)
-    if (tid == 0) s_lo = bound(xs, n, (double)v - cut, false);
-    else s_hi = bound(xs, n, (double)v + cut, true);
+    if (tid == 0) { s_lo = bound(xs, n, (double)v - cut, false); s_bmin = v; }
+    else { s_hi = bound(xs, n, (double)v + cut, true); s_bmax = v; }
   }
   __syncthreads();
   const int64_t lo = s_lo, hi = s_hi > s_lo ? s_hi : s_lo;
   const int64_t len = hi - lo;
   const int64_t jb = lo + len * s / S, je = lo + len * (s + 1) / S;
   const u64 k2 = pk2(kf, kf);
-  const float4* sx4 = reinterpret_cast<const float4*>(sx);
-
-  for (int64_t t0 = jb; t0 < je; t0 += kKdeTX) {
-    const int cnt = (int)((je - t0) < kKdeTX ? (je - t0) : kKdeTX);
-    __syncthreads();  // previous tile fully consumed
-    for (int q = tid; q < kKdeTX; q += kKdeThreads) sx[q] = (q < cnt) ? __ldg(xs + t0 + q) : 0.f;
-    __syncthreads();
-    const int full = cnt / kKdeCH;
-    for (int c = 0; c < full; ++c) {
-      u64 acc[kKdeRG];
+  const u64 sk2 = pk2(sk, sk);
+  // centred form when the block's points are close together (uniform across the CTA)
+  const float c = s_bmin;
+  const bool centred = KDE_CENTER && isfinite(c) && isfinite(s_bmax) && (s_bmax - c) * sk <= 2.5f;
+  u64 nP2[kKdeRG];
 #pragma unroll
-      for (int k = 0; k < kKdeRG; ++k) acc[k] = 0ull;
-#pragma unroll
-      for (int q = 0; q < kKdeCH / 4; ++q) {
-        const float4 v = sx4[c * (kKdeCH / 4) + q];
-        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
-#pragma unroll
-        for (int k = 0; k < kKdeRG; ++k) {
-          kde_term2(j01, p2[k], k2, acc[k]);
-          // hybrid: one term pair in four takes its exp on the FMA pipe (kHybFrac = 1/4)
-          if (HYB && (q & 1)) kde_term2_poly(j23, p2[k], k2, acc[k]);
-          else kde_term2(j23, p2[k], k2, acc[k]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kKdeRG; ++k) {
-        float a0, a1;
-        upk2(acc[k], a0, a1);
-        drow[k] += f32_to_f64_alu(a0 + a1);
-      }
-    }
-    if (full * kKdeCH < cnt) {  // ragged last chunk
-      u64 acc[kKdeRG];
-#pragma unroll
-      for (int k = 0; k < kKdeRG; ++k) acc[k] = 0ull;
-      for (int q = 0; q < kKdeCH / 4; ++q) {
-        const float4 v = sx4[full * (kKdeCH / 4) + q];
-        const int j = full * kKdeCH + 4 * q;
-        const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
-#pragma unroll
-        for (int k = 0; k < kKdeRG; ++k) {
-          kde_term2_masked(j01, p2[k], k2, acc[k], j < cnt, j + 1 < cnt);
-          kde_term2_masked(j23, p2[k], k2, acc[k], j + 2 < cnt, j + 3 < cnt);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kKdeRG; ++k) {
-        float a0, a1;
-        upk2(acc[k], a0, a1);
-        drow[k] += f32_to_f64_alu(a0 + a1);
-      }
-    }
+  for (int k = 0; k < kKdeRG; ++k) {
+    const float P = -__fmul_rn(__fsub_rn(pv[k], c), sk);
+    nP2[k] = pk2(P, P);
   }
+
+  if (centred) kde_tiles<HYB, true>(xs, jb, je, c, p2, nP2, k2, sk2, sx, drow);
+  else kde_tiles<HYB, false>(xs, jb, je, c, p2, nP2, k2, sk2, sx, drow);
 
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   const bool bad = ctrl->nonfinite != 0;
@@ -250,13 +315,14 @@ cudaError_t launch_kde(const float* xs, int64_t n, double h, const float* pts, i
   if (e != cudaSuccess) return e;
   const double kd = -1.4426950408889634074 / (2.0 * h * h);  // -log2(e) / (2 h^2)
   const float kf = (float)kd;
+  const float sk = (float)(sqrt(1.4426950408889634074 / 2.0) / h);  // sqrt(log2(e)/2) / h
   const double cut = sqrt(126.5 / fabs((double)kf)) * (1.0 + 1e-6);
   const double scale = kInvSqrt2Pi / ((double)n * h);
   if (kde_hybrid())
-    kde_kernel<true><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, cut, S, scale, ctrl, partial,
-                                                                    counters, f);
+    kde_kernel<true><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, sk, cut, S, scale, ctrl,
+                                                                    partial, counters, f);
   else
-    kde_kernel<false><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, cut, S, scale, ctrl,
+    kde_kernel<false><<<(unsigned int)(nb * S), kKdeThreads, 0, st>>>(xs, n, pts, m, kf, sk, cut, S, scale, ctrl,
                                                                      partial, counters, f);
   return cudaGetLastError();
 }
