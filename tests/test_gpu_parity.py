@@ -381,3 +381,14 @@ def test_sort_is_exact(P, n):
         x[-3:] = [3e38, -3e38, 0.5]
     got = P.plugin_sort(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), _key_sorted(x).view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [65023, 70001, 130047])
+def test_psi_r_at_every_tile_shape(P, oracle_mod, n):
+    # the tile edge T = 256 R switches with n (R = 1 below 65024, 2 up to 130047, then 4, 8):
+    # the R = 2 shape and both switch points against the oracle (a few 1e9 pairs, seconds)
+    x = inputs.mixture(n, 77)
+    for r, g in ((6, 0.4), (4, 0.15)):
+        got = P.psi_r(torch.from_numpy(x).cuda(), g, r).item()
+        ref = oracle_mod.psi(oracle_mod.widen(x), g, r)
+        assert rel(got, ref) < TOL, (n, r, got, ref)
