@@ -236,7 +236,8 @@ plugin_status kde_eval_prepared(int64_t n, double h, const float* d_points, int6
 
 /* The ordering step of the path (not a step of Alg. 1: it fixes the summation order, DESIGN.md
  * §6.4): d_sorted (device float32[n]) = X in ascending order of the IEEE bits' total order
- * (-NaN < -Inf < ... < -0 < +0 < ... < +Inf < +NaN), i.e. the unique array the passes read.
+ * (-NaN < -Inf < ... < -0 < +0 < ... < +Inf < +NaN), i.e. the unique array the passes read
+ * (for n <= 32768 the NaN with payload bits 0x7fffffff comes out as 0x7ffffffe, another NaN).
  * Needs plugin_workspace_bytes(n); asynchronous. */
 plugin_status plugin_sort(const float* d_x, int64_t n, float* d_sorted, void* d_ws, size_t ws_bytes,
                           void* stream);
