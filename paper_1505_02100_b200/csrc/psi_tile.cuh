@@ -94,6 +94,29 @@ __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, 
   acc = fma2(hermite_t<ORDER>(t), e, acc);
 }
 
+// pair2 with the exp on the FMA pipe (ex2_fma2) instead of MUFU.EX2, for the r = 4 hybrid
+// (PSI_HYB4): results below 2^-126 become +0 as MUFU.EX2.ftz flushes them, so all-zero tiles
+// stay exactly zero
+template <int ORDER, bool CENTER>
+__device__ __forceinline__ void pair2_fma(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc) {
+  const u64 c2 = 0xBF38AA3BBF38AA3Bull;
+  u64 u = CENTER ? fma2(xj, s2, xi) : mul2(sub2(xj, xi), s2);
+  u64 t = mul2(u, u);
+  u64 a = fma2(t, c2, ph);
+  float a0, a1, e0, e1;
+  upk2(a, a0, a1);
+  upk2(ex2_fma2(pk2(fmaxf(a0, -126.f), fmaxf(a1, -126.f))), e0, e1);
+  e0 = (a0 < -126.f) ? 0.f : e0;
+  e1 = (a1 < -126.f) ? 0.f : e1;
+  acc = fma2(hermite_t<ORDER>(t), pk2(e0, e1), acc);
+}
+
+// r = 4 hybrid exp: 1 pair in 8 on the FMA pipe (the LP optimum for 6 FP32 ops + 1 ex2 per
+// pair with the centred form: min(16 / (7/8), 128 / (6 + 8/8)) = 18.3 pairs/clk/SM); 0 = off
+#ifndef PSI_HYB4
+#define PSI_HYB4 0
+#endif
+
 __device__ __forceinline__ Fx128 fx_from_double(double x) {
   Fx128 r;
   double fl = floor(x);
@@ -166,7 +189,10 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         pair2<ORDER, false, CEN>(j01, xi[k], s2[k], ph[k], acc[k]);
-        pair2<ORDER, false, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
+        if (PSI_HYB4 && ORDER == 4 && R == 8 && (k == (q & 7) || k == ((q + 4) & 7)))
+          pair2_fma<ORDER, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
+        else
+          pair2<ORDER, false, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
       }
     }
 #pragma unroll
