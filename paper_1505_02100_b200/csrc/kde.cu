@@ -125,7 +125,8 @@ __device__ __forceinline__ void kde_tiles(const float* __restrict__ xs, int64_t 
             // hybrid: 5 term pairs in 16 take their exp on the FMA pipe (the LP optimum for
             // 3 + 8 FP32 ops)
             kde_term2_c(j01, nP2[k], sk2, acc[k]);
-            if (HYB && k < 2 + (q & 1)) kde_term2_c_poly(j23, nP2[k], sk2, acc[k]);
+            if (HYB && k < KDE_POLY16 / 2 + ((q & 1) ? (KDE_POLY16 & 1) : 0))
+              kde_term2_c_poly(j23, nP2[k], sk2, acc[k]);
             else kde_term2_c(j23, nP2[k], sk2, acc[k]);
           } else {
             kde_term2(j01, p2[k], k2, acc[k]);
@@ -174,6 +175,9 @@ __device__ __forceinline__ void kde_tiles(const float* __restrict__ xs, int64_t 
 
 #ifndef KDE_CENTER
 #define KDE_CENTER 1  // 0: difference-first terms everywhere (A/B builds)
+#endif
+#ifndef KDE_POLY16
+#define KDE_POLY16 5  // centred hybrid: term pairs in 16 with the FMA-pipe exp (<= 8)
 #endif
 
 // resident CTAs per SM the register budget is sized for (tuning: -DKDE_OCC=3 fits 78 registers)

@@ -112,7 +112,9 @@ __device__ __forceinline__ void pair2_fma(u64 xj, u64 xi, u64 s2, u64 ph, u64& a
 }
 
 // r = 4 hybrid exp: 1 pair in 8 on the FMA pipe (the LP optimum for 6 FP32 ops + 1 ex2 per
-// pair with the centred form: min(16 / (7/8), 128 / (6 + 8/8)) = 18.3 pairs/clk/SM); 0 = off
+// pair with the centred form: min(16 / (7/8), 128 / (6 + 8/8)) = 18.3 pairs/clk/SM); 0 = off:
+// measured 4.24e12 vs 4.48e12 pairs/s (profiles/r01u_*) -- two saturated pipes interleave worse
+// than one
 #ifndef PSI_HYB4
 #define PSI_HYB4 0
 #endif
