@@ -26,6 +26,13 @@
 
 namespace plg {
 
+#ifndef KDE_CENTER
+#define KDE_CENTER 1  // 0: difference-first terms everywhere (A/B builds)
+#endif
+#ifndef KDE_POLY16
+#define KDE_POLY16 5  // centred hybrid: term pairs in 16 with the FMA-pipe exp (<= 8)
+#endif
+
 constexpr int kKdeThreads = 256;
 constexpr int kKdeRG = 4;                      // points per thread
 constexpr int kKdeGB = kKdeThreads * kKdeRG;   // points per block
@@ -173,12 +180,6 @@ __device__ __forceinline__ void kde_tiles(const float* __restrict__ xs, int64_t 
 
 }
 
-#ifndef KDE_CENTER
-#define KDE_CENTER 1  // 0: difference-first terms everywhere (A/B builds)
-#endif
-#ifndef KDE_POLY16
-#define KDE_POLY16 5  // centred hybrid: term pairs in 16 with the FMA-pipe exp (<= 8)
-#endif
 
 // resident CTAs per SM the register budget is sized for (tuning: -DKDE_OCC=3 fits 78 registers)
 #ifndef KDE_OCC
