@@ -456,11 +456,10 @@ def run_kde(a):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
     mufu_only = os.environ.get("PLUGIN_KDE_MUFU_ONLY") == "1"
-    # MUFU-only: 16 ex2/clk/SM.  Hybrid (default): 11 of 16 terms on MUFU (3 FP32 lane-ops each),
-    # 5 of 16 with an 8-lane-op FMA-pipe exp2: min(16 / (11/16), 128 / (3 + 8 * 5/16)) = 23.27 terms/clk/SM
-    # centred terms (3 FP32 ops + 1 ex2) with 5/16 FMA-pipe exps: 16 / (11/16) = 23.27;
-    # the difference-first fallback (4 ops, 1/4 FMA-pipe exps) is bound at 21.33
-    per_clk = MUFU_EX2_PER_CLK_PER_SM if mufu_only else 16.0 / (11.0 / 16.0)
+    # MUFU-only: 16 ex2/clk/SM.  Hybrid (default, centred terms of 3 FP32 lane-ops):
+    # 12 of 16 terms on MUFU, 4 of 16 with an 8-lane-op FMA-pipe exp2:
+    # min(16 / (12/16), 128 / (3 + 8 * 4/16)) = 21.33 terms/clk/SM (MUFU-bound)
+    per_clk = MUFU_EX2_PER_CLK_PER_SM if mufu_only else 16.0 / (12.0 / 16.0)
     peak = per_clk * sms * f_meas * 1e6 / 1e9
     achieved = visited / (k_ms / 1e3) / 1e9
     # end to end from host memory: H2D of X and the points, D2H of the curve
@@ -488,8 +487,8 @@ def run_kde(a):
                          "kernel_ms": k_ms, "prepare_ms": ms - k_ms,
                          "peak_basis": (f"{per_clk:.2f} terms/clk/SM x {sms} SMs x {f_meas:.0f} MHz ("
                                         + ("MUFU.EX2-bound, 1 ex2 per visited term" if mufu_only else
-                                           "MUFU + FMA pipes saturated together: 11/16 of the exps on MUFU.EX2, "
-                                           "5/16 on the FMA pipe, centred terms") + ")"),
+                                           "12/16 of the exps on MUFU.EX2 (the binding pipe), 4/16 on the FMA "
+                                           "pipe, centred terms") + ")"),
                          "variant": "mufu_only" if mufu_only else "hybrid"},
             "e2e": {"value": n * m / statistics.median(ts) / 1e9, "unit": "GTerms/s",
                     "h2d_bytes_per_step": 4 * (n + m), "d2h_bytes_per_step": 8 * m,

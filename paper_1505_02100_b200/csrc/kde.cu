@@ -30,7 +30,7 @@ namespace plg {
 #define KDE_CENTER 1  // 0: difference-first terms everywhere (A/B builds)
 #endif
 #ifndef KDE_POLY16
-#define KDE_POLY16 5  // centred hybrid: term pairs in 16 with the FMA-pipe exp (<= 8)
+#define KDE_POLY16 4  // centred hybrid: term pairs in 16 with the FMA-pipe exp (<= 8; A/B: 4 best)
 #endif
 
 constexpr int kKdeThreads = 256;
@@ -129,8 +129,8 @@ __device__ __forceinline__ void kde_tiles(const float* __restrict__ xs, int64_t 
 #pragma unroll
         for (int k = 0; k < kKdeRG; ++k) {
           if (CEN) {
-            // hybrid: 5 term pairs in 16 take their exp on the FMA pipe (the LP optimum for
-            // 3 + 8 FP32 ops)
+            // hybrid: KDE_POLY16 term pairs in 16 take their exp on the FMA pipe (DESIGN.md §10:
+            // the LP optimum of 3 + 8 FP32 ops is 5, measured best 4 -- MUFU-bound, FMA slack)
             kde_term2_c(j01, nP2[k], sk2, acc[k]);
             if (HYB && k < KDE_POLY16 / 2 + ((q & 1) ? (KDE_POLY16 & 1) : 0))
               kde_term2_c_poly(j23, nP2[k], sk2, acc[k]);
