@@ -21,7 +21,7 @@
 // k_i in [-7, 7], decorrelates the fp32 rounding of u and t across rows (matters for
 // discretised samples with few distinct differences); it is a zero-mean dilation of
 // <= 1e-6 whose effect is second order.
-// fp32 accumulators hold 16 terms per lane, then go to per-row fp64; each tile's fp64
+// fp32 accumulators hold 32 terms per lane (64 per row, PSI_CH), then go to per-row fp64; each tile's fp64
 // total is added as a 128-bit fixed-point integer, so the result does not depend on
 // tile scheduling, grid size or GPU count.
 #include <cstdlib>
