@@ -57,29 +57,32 @@ __device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
 }
 
 // 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff, real keys
-// <= 0xfffffffe -- see blocksort_key).  On return out[0 .. 2048) holds the ascending array; a
-// (2048 words of shared memory) is scratch.  After the warp sorts, three rounds of pairwise
-// merges by rank (runs of 256 -> 512 -> 1024 -> 2048): a key's position in the merged run is its
-// index in its run plus the keys of the partner run below it (an earlier partner counts equal
-// keys too, so positions are unique): one branch-free binary search per key per round.
-// Contains __syncthreads().
-__device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* a, unsigned int* out) {
+// <= 0xfffffffe -- see blocksort_key), cnt <= 2048 of them real (positions < cnt).  On return
+// out[0 .. cnt) holds the ascending array; a (2048 words of shared memory) is scratch.  After
+// the warp sorts, rounds of pairwise merges by rank (runs of 256 -> 512 -> 1024 -> 2048, only as
+// many as the cnt keys need): a key's position in the merged run is its index in its run plus
+// the keys of the partner run below it (an earlier partner counts equal keys too, so positions
+// are unique): one branch-free binary search per key per round.  Contains __syncthreads().
+__device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* a, unsigned int* out, int cnt) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  warp_sort256(k);
+  int lgmax = 8;  // runs of 2^lgmax cover the cnt keys
+  while ((1 << lgmax) < cnt) ++lgmax;
+  const int active = 1 << lgmax;  // positions that take part (the rest are pads)
+  if ((w << 8) < active) warp_sort256(k);  // runs of pads only are sorted already
+  unsigned int* src = (lgmax - 8) & 1 ? a : out;  // the last round writes out
+  unsigned int* dst = (lgmax - 8) & 1 ? out : a;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) a[(w << 8) + (lane << 3) + r] = k[r];
+  for (int r = 0; r < 8; ++r) src[(w << 8) + (lane << 3) + r] = k[r];
   __syncthreads();
-  unsigned int* src = a;
-  unsigned int* dst = out;
 #pragma unroll 1
-  for (int lg = 8; lg < 11; ++lg) {  // run length L = 2^lg
+  for (int lg = 8; lg < lgmax; ++lg) {  // run length L = 2^lg
     const int L = 1 << lg;
     // the thread's 8 keys search in lockstep: 8 independent shared-memory loads per step
     unsigned int v[8], t[8];
     int pos[8], base[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int p = (tid << 3) + r;
+      const int p = ((tid << 3) + r) & (active - 1);  // threads past `active` redo a key (same write)
       v[r] = src[p];
       const int run = p >> lg;
       const bool later = run & 1;                 // the partner run comes first
@@ -98,7 +101,7 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int p = (tid << 3) + r;
+      const int p = ((tid << 3) + r) & (active - 1);
       const int run = p >> lg, i = p & (L - 1);
       const int ps = ((run & 1) && v[r] == 0xffffffffu) ? L : pos[r];  // a pad after the partner run
       dst[((run & ~1) << lg) + i + ps] = v[r];
@@ -108,7 +111,7 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
     src = dst;
     dst = tmp;
   }
-  // three rounds: the result is in out (src after the last swap)
+  // lgmax - 8 rounds: the result is in out (src after the last swap)
 }
 
 // the sort key of a float's bits, with the NaN 0x7fffffff folded onto 0x7ffffffe (another NaN)

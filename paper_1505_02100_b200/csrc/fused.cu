@@ -71,7 +71,7 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
       const int i = 8 * tid + r;
       k[r] = (i < n) ? blocksort_key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
     }
-    cta_sort2048(k, key + nsx, key);  // runs: the 2048 words after the sample
+    cta_sort2048(k, key + nsx, key, (int)n);  // runs: the 2048 words after the sample
   }
   FT_MARK(1);
   for (int i = tid; i < n; i += kPsiThreads) key[i] = key2bits(key[i]);

@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict
     const int64_t i = base + 8 * threadIdx.x + r;
     k[r] = (i < n) ? blocksort_key(__ldg(reinterpret_cast<const unsigned int*>(x) + i)) : 0xffffffffu;
   }
-  cta_sort2048(k, runs, out);
   const int cnt = (int)((n - base) < kBlockSortN ? (n - base) : kBlockSortN);
+  cta_sort2048(k, runs, out, cnt);
   if (gridDim.x == 1) {
     for (int i = threadIdx.x; i < cnt; i += 256) reinterpret_cast<unsigned int*>(xs)[i] = key2bits(out[i]);
   } else {
