@@ -4,10 +4,9 @@
 //  * warp_sort256: a warp sorts 256 keys held 8 per lane in registers (bitonic network;
 //    strides < 8 inside a lane, strides >= 8 across lanes by __shfl_xor_sync) -- no shared
 //    memory, no barriers, no branches;
-//  * cta_sort2048: 8 warps sort 8 runs of 256, then 3 rounds of pairwise merges by rank
-//    (branch-free binary searches in shared memory; a partner run that comes first counts
-//    equal keys too, so positions are unique).  Equal keys are identical bit patterns, so the
-//    output is THE ascending array (the same one the radix sort produces);
+//  * cta_sort2048: 8 warps sort 8 runs of 256, then up to 3 rounds of pairwise merge-path
+//    merges in shared memory.  Equal keys are identical bit patterns, so the output is THE
+//    ascending array (the same one the radix sort produces);
 //  * across CTAs (sort.cu): a rank merge over sorted blocks of 2048 in global memory.
 // The routines run once per launch, so the loops stay rolled: fully unrolled they were ~10k
 // instructions fetched cold from L2 (measured 26 us for 2048 keys).
@@ -59,10 +58,10 @@ __device__ __forceinline__ void warp_sort256(unsigned int (&k)[8]) {
 // 256 threads: k[8] are this thread's 8 keys (positions 8 * tid ..; pads 0xffffffff, real keys
 // <= 0xfffffffe -- see blocksort_key), cnt <= 2048 of them real (positions < cnt).  On return
 // out[0 .. cnt) holds the ascending array; a (2048 words of shared memory) is scratch.  After
-// the warp sorts, rounds of pairwise merges by rank (runs of 256 -> 512 -> 1024 -> 2048, only as
-// many as the cnt keys need): a key's position in the merged run is its index in its run plus
-// the keys of the partner run below it (an earlier partner counts equal keys too, so positions
-// are unique): one branch-free binary search per key per round.  Contains __syncthreads().
+// the warp sorts, rounds of pairwise merges (runs of 256 -> 512 -> 1024 -> 2048, only as many as
+// the cnt keys need) by merge path: each thread finds where its 8 output positions split the
+// two runs (one binary search on the diagonal) and merges them sequentially.
+// Contains __syncthreads().
 __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int* a, unsigned int* out, int cnt) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   int lgmax = 8;  // runs of 2^lgmax cover the cnt keys
@@ -75,36 +74,29 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
   for (int r = 0; r < 8; ++r) src[(w << 8) + (lane << 3) + r] = k[r];
   __syncthreads();
 #pragma unroll 1
-  for (int lg = 8; lg < lgmax; ++lg) {  // run length L = 2^lg
+  for (int lg = 8; lg < lgmax; ++lg) {  // runs of L = 2^lg merged pairwise (merge path)
     const int L = 1 << lg;
-    // the thread's 8 keys search in lockstep: 8 independent shared-memory loads per step
-    unsigned int v[8], t[8];
-    int pos[8], base[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = ((tid << 3) + r) & (active - 1);  // threads past `active` redo a key (same write)
-      v[r] = src[p];
-      const int run = p >> lg;
-      const bool later = run & 1;                 // the partner run comes first
-      t[r] = later ? v[r] + 1u : v[r];            // count keys < t; v + 1 wraps only for pads
-      base[r] = (run ^ 1) << lg;
-      pos[r] = 0;
-    }
-#pragma unroll 1
-    for (int step = L; step > 0; step >>= 1) {  // counts 0 .. L
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int idx = pos[r] + step - 1;
-        const unsigned int x = src[base[r] + (idx < L ? idx : L - 1)];
-        pos[r] += (idx < L && x < t[r]) ? step : 0;
+    const int o = tid << 3;  // this thread writes merged positions o .. o + 7
+    if (o < active) {
+      const int base = (o >> (lg + 1)) << (lg + 1), d = o & (2 * L - 1);
+      const unsigned int* A = src + base;
+      const unsigned int* B = A + L;
+      // split of the diagonal d: i keys from A, d - i from B (ties: A first)
+      int lo = d > L ? d - L : 0, hi = d < L ? d : L;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d - mid - 1]) lo = mid + 1;
+        else hi = mid;
       }
-    }
+      int i = lo, j = d - lo;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = ((tid << 3) + r) & (active - 1);
-      const int run = p >> lg, i = p & (L - 1);
-      const int ps = ((run & 1) && v[r] == 0xffffffffu) ? L : pos[r];  // a pad after the partner run
-      dst[((run & ~1) << lg) + i + ps] = v[r];
+      for (int q = 0; q < 8; ++q) {
+        const unsigned int av = i < L ? A[i] : 0xffffffffu, bv = j < L ? B[j] : 0xffffffffu;
+        const bool ta = i < L && (j >= L || av <= bv);
+        dst[base + d + q] = ta ? av : bv;
+        i += ta ? 1 : 0;
+        j += ta ? 0 : 1;
+      }
     }
     __syncthreads();
     unsigned int* tmp = src;
