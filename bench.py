@@ -43,10 +43,11 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--workload", default="plugin", choices=["plugin", "kde", "q32", "dpi"],
+    ap.add_argument("--workload", default="plugin", choices=["plugin", "kde", "q32", "dpi", "batch"],
                     help="plugin: Alg. 1 (the headline); kde: Eq. 1-2 on a 65536-point curve (NEXT 1); "
                          "q32: Alg. 1 with the Q32.32 pair passes (NEXT 2); dpi: the l-stage plug-in (NEXT 3)")
     ap.add_argument("--stages", type=int, default=3, help="dpi workload: l")
+    ap.add_argument("--batch", type=int, default=4096, help="batch workload: samples of n = 1024")
     ap.add_argument("--kde-points", type=int, default=65536)
     ap.add_argument("--skip-underflow", action="store_true",
                     help="plugin workload, 1 GPU: PLUGIN_SKIP_UNDERFLOW (bit-identical result; reports the "
@@ -552,6 +553,58 @@ def run_variant(a):
     return 0
 
 
+def run_batch(a):
+    """plugin_h_batch over a.batch independent N(0,1) samples of n = 1024 (the paper's largest
+    size, Table 2): whole-algorithm throughput for many small problems, one CTA per sample."""
+    import numpy as np
+    import torch
+
+    from paper_1505_02100_b200 import plugin as P
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n, count = 1024, a.batch
+    xh = np.random.default_rng(123).standard_normal(n * count).astype(np.float32)
+    x = torch.from_numpy(xh).to(dev)
+    offs = torch.arange(0, n * (count + 1), n, dtype=torch.int64, device=dev)
+    out = torch.empty(count * P.RESULT_BYTES, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(a.warmup):
+        P.plugin_h_batch(x, offs, out=out)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    for s in range(a.steps):
+        flush.fill_(s & 0xff)
+        ev[s][0].record(stream)
+        P.plugin_h_batch(x, offs, out=out)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in ev])
+    pairs = count * n * (n - 1)  # both passes, unique pairs
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_meas = clocks.get("sm_mhz") or 1965.0
+    peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
+    # the batch kernel evaluates the diagonal tiles as full squares: (n + T)(n) / 2 per pass, T = 64
+    evaluated = count * 2 * (n * (n + 64) // 2)
+    res = P.read_results(out, 2)
+    line = {"metric": "pairwise K4/K6 evaluations/sec, batches of independent samples", "value": pairs / (ms / 1e3) / 1e9,
+            "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"plugin_h_batch: {count} samples of n = {n} N(0,1), full PLUGIN each",
+                       "us_per_sample": ms * 1e3 / count, "pairs_per_step": pairs},
+            "roofline": {"bound": "alu", "achieved": evaluated / (ms / 1e3) / 1e9, "peak": peak, "unit": UNIT,
+                         "frac": evaluated / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "kernel": "plugin_batch_kernel (whole step)",
+                         "peak_basis": f"{MUFU_EX2_PER_CLK_PER_SM} MUFU.EX2/clk/SM x {sms} SMs x {f_meas:.0f} MHz"},
+            "h_first": res[0]["h"], "status_first": res[0]["status"], "clocks": clocks, "gpu_launches": a.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     a = _args()
     if a.impl == "reference":
@@ -560,6 +613,8 @@ def main():
         return run_kde(a)
     if a.workload in ("q32", "dpi"):
         return run_variant(a)
+    if a.workload == "batch":
+        return run_batch(a)
     if a.skip_underflow:
         return run_skip(a)
     return run_ours(a)

@@ -102,6 +102,15 @@ plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
 plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, unsigned int flags,
                           void* d_ws, size_t ws_bytes, void* stream);
 
+/* Many independent small samples in one launch (throughput for batches of the paper's sizes):
+ * sample b is d_x[d_offsets[b] .. d_offsets[b+1]) (device float32 / int64[count + 1], ascending
+ * offsets), 2 <= n_b <= 2048; d_out[b] (device plugin_result[count]) receives Algorithm 1 for it,
+ * bit-identical to plugin_h on that sample alone.  A sample outside [2, 2048] gets status
+ * PLUGIN_E_INVALID in its result.  One CTA per sample, no workspace.  flags: 0 or
+ * PLUGIN_SKIP_UNDERFLOW.  Asynchronous. */
+plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int count, plugin_result* d_out,
+                             unsigned int flags, void* stream);
+
 /* Same as plugin_h (device result kept in the workspace), then synchronises `stream`,
  * copies the result to *h_out and returns its data status (PLUGIN_OK or one of
  * E_NONFINITE/E_DEGENERATE/E_DOMAIN). */

@@ -265,6 +265,19 @@ plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_ou
   return after(1, d_total, d_out, stream);
 }
 
+plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int count, plugin_result* d_out,
+                             unsigned int flags, void* stream) {
+  g_err[0] = 0;
+  if (count < 0) return fail(PLUGIN_E_INVALID, "count must be >= 0%s");
+  if (count == 0) return PLUGIN_OK;
+  if (!d_x || !d_offsets || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  if (flags & ~(unsigned int)PLUGIN_SKIP_UNDERFLOW) return fail(PLUGIN_E_INVALID, "unknown flags%s");
+  cudaError_t e = launch_batch(d_x, d_offsets, count, (flags & PLUGIN_SKIP_UNDERFLOW) ? 1 : 0, d_out,
+                               static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "batch");
+  return PLUGIN_OK;
+}
+
 plugin_status plugin_sort(const float* d_x, int64_t n, float* d_sorted, void* d_ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   if (!d_x || !d_sorted) return fail(PLUGIN_E_INVALID, "null pointer argument%s");

@@ -92,6 +92,9 @@ cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
 // 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
 constexpr int kFusedMaxGrid = 1024;
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s);
+// many samples of 2 <= n_b <= kFusedMaxN, one CTA each (fused.cu): offsets[count + 1] on the device
+cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int skip, plugin_result* out,
+                         cudaStream_t s);
 // the Q32.32 datapath (q32.cu): one pass over the Q32.32 sample zq with rg from rg_dev (or
 // rg_host), its exact 128-bit total to out[2] (if out) and, with res, the PLUGIN finalize of
 // pass `what` (rg_next <- encode(1/g2_z) after pass 0)

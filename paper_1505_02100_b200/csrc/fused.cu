@@ -48,21 +48,14 @@ __device__ __forceinline__ Fx128 ldcg_fx(const Fx128* p) {
   return r;
 }
 
-template <int R>
-__global__ void __launch_bounds__(kPsiThreads)
-plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, plugin_result* out, Fx128* parts) {
-  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded; then sort scratch
-  __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
-  __shared__ int sh_bad[8];
-  __shared__ double p1[2 * 8];
-  __shared__ plugin_result res;
-  __shared__ Fx128 fx_red[kPsiThreads / 32];
-  static_assert(R == 0, "the fused path uses the small tiles of psi_tile.cuh");
-  constexpr int T = kPsiSmallT;
+// Every CTA of a single-sample launch (and each CTA of a batch): the sorted sample in shared
+// memory (padded to nsx with its largest value) and Steps I-III in res, with the reduction tree
+// of step1_kernel.  Contains __syncthreads().
+__device__ __forceinline__ void cta_prologue(const float* __restrict__ x, int64_t n, int nsx, float* xsm,
+                                             plugin_result* res, double* sh1, double* sh2, int* sh_bad,
+                                             double* p1) {
   unsigned int* key = reinterpret_cast<unsigned int*>(xsm);
   const int tid = threadIdx.x;
-
-  FT_MARK(0);
   // sort (keys of the raw bits: pads are 0xffffffff and sort last): blocksort.cuh, n <= 2048
   {
     unsigned int k[8];
@@ -73,12 +66,11 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
     }
     cta_sort2048(k, key + nsx, key, (int)n);  // runs: the 2048 words after the sample
   }
-  FT_MARK(1);
   for (int i = tid; i < n; i += kPsiThreads) key[i] = key2bits(key[i]);
   __syncthreads();
   const float xpad = xsm[n - 1];
   for (int64_t i = n + tid; i < nsx; i += kPsiThreads) xsm[i] = xpad;
-  if (tid == 0) init_result(&res, n);
+  if (tid == 0) init_result(res, n);
   __syncthreads();
 
   // Step I (+ II, III) with step1_kernel's reduction tree over step1_grid(n) blocks
@@ -95,10 +87,28 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
   if (tid < 32) {
     double a, q;
     step1_total<false>(p1, nb1, a, q);
-    if (tid == 0) step1_epilogue(a, q, n, K, bad != 0, &res);
+    if (tid == 0) step1_epilogue(a, q, n, K, bad != 0, res);
   }
   __syncthreads();
+}
 
+template <int R>
+__global__ void __launch_bounds__(kPsiThreads)
+plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, plugin_result* out, Fx128* parts) {
+  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded; then sort scratch
+  __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
+  __shared__ int sh_bad[8];
+  __shared__ double p1[2 * 8];
+  __shared__ plugin_result res;
+  __shared__ Fx128 fx_red[kPsiThreads / 32];
+  static_assert(R == 0, "the fused path uses the small tiles of psi_tile.cuh");
+  constexpr int T = kPsiSmallT;
+  const int tid = threadIdx.x;
+
+  FT_MARK(0);
+  cta_prologue(x, n, nsx, xsm, &res, sh1, sh2, sh_bad, p1);
+  FT_MARK(1);
+  const float xpad = xsm[n - 1];
   FT_MARK(2);
   // Steps IV/V and VI/VII
   cg::grid_group grid = cg::this_grid();
@@ -150,6 +160,75 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
     FT_MARK(5 + 3 * pass);
   }
   if (blockIdx.x == 0 && tid == 0) *out = res;
+}
+
+// Many small samples in one launch (plugin_h_batch): CTA b runs the whole algorithm for sample
+// b (2 <= n_b <= 2048) on its own -- no grid barrier: the prologue above, then every tile of each
+// pass by this CTA, the same tile sums, the same order-free 128-bit total and the same
+// finalize, so each result is bit-identical to plugin_h on that sample alone.
+__global__ void __launch_bounds__(kPsiThreads)
+plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets, int count, int skip,
+                    plugin_result* __restrict__ out) {
+  extern __shared__ __align__(16) float xsm[];  // 2048 sample + 2048 sort scratch
+  __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
+  __shared__ int sh_bad[8];
+  __shared__ double p1[2 * 8];
+  __shared__ plugin_result res;
+  constexpr int T = kPsiSmallT;
+  const int tid = threadIdx.x;
+  for (int b = blockIdx.x; b < count; b += gridDim.x) {
+    const int64_t o0 = offsets[b], n = offsets[b + 1] - o0;
+    if (n < 2 || n > kFusedMaxN) {  // not a sample this path takes: E_INVALID in its result
+      if (tid == 0) {
+        init_result(&out[b], n);
+        out[b].status = PLUGIN_E_INVALID;
+      }
+      continue;
+    }
+    const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
+    const int nsx = (int)(nb * T > kBlockSortN ? nb * T : kBlockSortN);
+    __syncthreads();  // the previous sample's shared data is consumed
+    cta_prologue(x + o0, n, nsx, xsm, &res, sh1, sh2, sh_bad, p1);
+    const float xpad = xsm[n - 1];
+    for (int pass = 0; pass < 2; ++pass) {
+      if (res.status != PLUGIN_OK) break;  // uniform: shared
+      const float s = __double2float_rn(1.0 / (pass == 0 ? res.g1 : res.g2));
+      Fx128 acc = {0ull, 0ll};
+      for (int64_t t = 0; t < tiles; ++t) {
+        int64_t bi, bj;
+        tile_coords(t, nb, bi, bj);
+        const int64_t i0 = bi * T, j0 = bj * T;
+        if (skip && bi != bj &&
+            ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
+          continue;
+        const int jcount = (int)((n - j0) < T ? (n - j0) : T);
+        const double w = (bi == bj) ? 1.0 : 2.0;
+        const double tt = (pass == 0) ? psi_tile_sum_small<6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
+                                      : psi_tile_sum_small<4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
+        if (tid == 0) fx_add(acc, fx_from_double(tt));
+      }
+      if (tid == 0) finalize_pass(pass, fx_to_double(acc), n, &res);
+      __syncthreads();
+    }
+    if (tid == 0) out[b] = res;
+  }
+}
+
+cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int skip, plugin_result* out,
+                         cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_batch_kernel, kPsiThreads,
+                                                  sizeof(float) * 2 * kBlockSortN);
+    max_grid = sms * (occ > 0 ? occ : 1);
+  }
+  const int grid = count < max_grid ? count : max_grid;
+  plugin_batch_kernel<<<grid, kPsiThreads, sizeof(float) * 2 * kBlockSortN, s>>>(x, offsets, count, skip, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {

@@ -74,6 +74,7 @@ def lib():
             "plugin_h": (i32, [P, i64, P, P, sz, P]),
             "plugin_h_ex": (i32, [P, i64, P, ctypes.c_uint, P, sz, P]),
             "plugin_h_sync": (i32, [P, i64, P, P, sz, P]),
+            "plugin_h_batch": (i32, [P, P, i32, P, ctypes.c_uint, P]),
             "plugin_h_host": (i32, [P, i64, P, P, sz, P]),
             "psi_r": (i32, [P, i64, d, i32, P, P, sz, P]),
             "plugin_step1": (i32, [P, i64, P, P, sz, P]),
@@ -105,7 +106,8 @@ def lib():
 PLUGIN_SKIP_UNDERFLOW = 1
 PLUGIN_MULTI_KERNEL = 2
 
-EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_sync", "plugin_h_host",
+EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_batch",
+            "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
             "plugin_shard_tiles", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
             "kde_workspace_bytes", "kde_eval", "kde_prepare",
@@ -169,6 +171,26 @@ def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor 
     _check(lib().plugin_h_ex(x.data_ptr(), n, out.data_ptr(), int(flags), ws.data_ptr(), ws.numel(),
                              _stream(stream)))
     return out
+
+
+def plugin_h_batch(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None, stream=None,
+                   flags: int = 0) -> torch.Tensor:
+    """Alg. 1 for every sample x[offsets[b]:offsets[b+1]] (2 <= n_b <= 2048), one CTA each;
+    returns the device buffer of count plugin_result records (read_results decodes it)."""
+    x = _x(x)
+    if not (isinstance(offsets, torch.Tensor) and offsets.is_cuda and offsets.dtype == torch.int64):
+        raise TypeError("offsets must be a CUDA int64 tensor of count + 1 entries")
+    offsets = offsets.contiguous()
+    count = offsets.numel() - 1
+    out = torch.empty(max(count, 1) * RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
+    _check(lib().plugin_h_batch(x.data_ptr(), offsets.data_ptr(), count, out.data_ptr(), int(flags),
+                                _stream(stream)))
+    return out
+
+
+def read_results(buf: torch.Tensor, count: int) -> list[dict]:
+    h = buf.detach().to("cpu").numpy().tobytes()
+    return [plugin_result.from_buffer_copy(h[k * RESULT_BYTES:(k + 1) * RESULT_BYTES]).to_dict() for k in range(count)]
 
 
 def plugin_h_sync(x: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> dict:

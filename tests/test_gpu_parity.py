@@ -392,3 +392,29 @@ def test_psi_r_at_every_tile_shape(P, oracle_mod, n):
         got = P.psi_r(torch.from_numpy(x).cuda(), g, r).item()
         ref = oracle_mod.psi(oracle_mod.widen(x), g, r)
         assert rel(got, ref) < TOL, (n, r, got, ref)
+
+
+def test_batch_bit_identical_to_single_runs(P):
+    # plugin_h_batch: one CTA per sample, each result bit-identical to plugin_h on the sample
+    rng = np.random.default_rng(11)
+    sizes = [2, 3, 64, 65, 128, 300, 1000, 1024, 1500, 2048, 1, 2049, 700]
+    samples = []
+    for k, n in enumerate(sizes):
+        x = inputs.mixture(n, 600 + k) if n > 3 else inputs.normal(n, 600 + k)
+        samples.append(x.astype(np.float32))
+    samples.append(np.full(500, 2.5, np.float32))                       # degenerate
+    bad = inputs.normal(400, 3)
+    bad[7] = np.nan
+    samples.append(bad)                                                  # non-finite
+    offs = np.cumsum([0] + [s.size for s in samples]).astype(np.int64)
+    x = torch.from_numpy(np.concatenate(samples)).cuda()
+    res = P.read_results(P.plugin_h_batch(x, torch.from_numpy(offs).cuda()), len(samples))
+    for s, r in zip(samples, res):
+        if s.size < 2 or s.size > 2048:
+            assert r["status"] == P.PLUGIN_E_INVALID
+            continue
+        one = P.read_result(P.plugin_h(torch.from_numpy(s).cuda()))
+        assert _same(one, r), (s.size, one, r)
+    assert res[-2]["status"] == P.PLUGIN_E_DEGENERATE and res[-1]["status"] == P.PLUGIN_E_NONFINITE
+    empty = P.plugin_h_batch(x, torch.zeros(1, dtype=torch.int64, device="cuda"))
+    assert empty.numel() == P.RESULT_BYTES

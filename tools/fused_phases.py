@@ -14,7 +14,7 @@ import torch  # noqa: E402
 from paper_1505_02100_b200 import inputs  # noqa: E402
 from paper_1505_02100_b200 import plugin as P  # noqa: E402
 
-NAMES = ["sort", "step1", "pass6", "sync6", "final6", "pass4", "sync4", "final4"]
+NAMES = ["sort_step1", "setup", "pass6", "sync6", "final6", "pass4", "sync4", "final4"]
 
 
 def main():
