@@ -104,8 +104,9 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
 
 /* Many independent small samples in one launch (throughput for batches of the paper's sizes):
  * sample b is d_x[d_offsets[b] .. d_offsets[b+1]) (device float32 / int64[count + 1], ascending
- * offsets), 2 <= n_b <= 2048; d_out[b] (device plugin_result[count]) receives Algorithm 1 for it,
- * bit-identical to plugin_h on that sample alone.  A sample outside [2, 2048] gets status
+ * offsets), 2 <= n_b <= 2048; d_out[b] (device plugin_result[count]) receives Algorithm 1 for it
+ * (the same Step I as plugin_h; the passes use larger tiles, so psi/h agree with plugin_h to fp32
+ * evaluation rounding, not bit for bit).  A sample outside [2, 2048] gets status
  * PLUGIN_E_INVALID in its result.  One CTA per sample, no workspace.  flags: 0 or
  * PLUGIN_SKIP_UNDERFLOW.  Asynchronous. */
 plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int count, plugin_result* d_out,

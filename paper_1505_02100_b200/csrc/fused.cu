@@ -163,18 +163,22 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
 }
 
 // Many small samples in one launch (plugin_h_batch): CTA b runs the whole algorithm for sample
-// b (2 <= n_b <= 2048) on its own -- no grid barrier: the prologue above, then every tile of each
-// pass by this CTA, the same tile sums, the same order-free 128-bit total and the same
-// finalize, so each result is bit-identical to plugin_h on that sample alone.
-__global__ void __launch_bounds__(kPsiThreads)
+// b (2 <= n_b <= 2048) on its own -- no grid barrier: the prologue above (the same sort and
+// Step I as plugin_h), then each pass over tiles of T = 1024 (R = 4 rows per thread, the
+// centred form of psi.cu: a whole sample is 1-3 tiles, ~2^20 pairs per tile, where the small
+// tiles of the latency path would be overhead-bound) and the same finalize.  The tiles differ
+// from plugin_h's, so results agree with it to fp32 evaluation rounding, not bit for bit.
+constexpr int kBatchR = 4, kBatchT = kPsiThreads * kBatchR;
+
+__global__ void __launch_bounds__(kPsiThreads, 2)
 plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets, int count, int skip,
                     plugin_result* __restrict__ out) {
-  extern __shared__ __align__(16) float xsm[];  // 2048 sample + 2048 sort scratch
+  extern __shared__ __align__(16) float xsm[];  // 2048 sample + 2048 sort scratch (reused as the j tile)
   __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
   __shared__ int sh_bad[8];
   __shared__ double p1[2 * 8];
   __shared__ plugin_result res;
-  constexpr int T = kPsiSmallT;
+  constexpr int T = kBatchT;
   const int tid = threadIdx.x;
   for (int b = blockIdx.x; b < count; b += gridDim.x) {
     const int64_t o0 = offsets[b], n = offsets[b + 1] - o0;
@@ -186,10 +190,10 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
       continue;
     }
     const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
-    const int nsx = (int)(nb * T > kBlockSortN ? nb * T : kBlockSortN);
     __syncthreads();  // the previous sample's shared data is consumed
-    cta_prologue(x + o0, n, nsx, xsm, &res, sh1, sh2, sh_bad, p1);
+    cta_prologue(x + o0, n, kBlockSortN, xsm, &res, sh1, sh2, sh_bad, p1);
     const float xpad = xsm[n - 1];
+    float* sx = xsm + kBlockSortN;  // the staged (centred) j block of a tile
     for (int pass = 0; pass < 2; ++pass) {
       if (res.status != PLUGIN_OK) break;  // uniform: shared
       const float s = __double2float_rn(1.0 / (pass == 0 ? res.g1 : res.g2));
@@ -202,9 +206,12 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
             ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
           continue;
         const int jcount = (int)((n - j0) < T ? (n - j0) : T);
+        const float cen = PSI_CENTER ? xsm[i0] : 0.f;
+        __syncthreads();  // sx of the previous tile consumed
+        for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((j0 + q < n) ? xsm[j0 + q] : xpad, cen);
         const double w = (bi == bj) ? 1.0 : 2.0;
-        const double tt = (pass == 0) ? psi_tile_sum_small<6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
-                                      : psi_tile_sum_small<4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
+        const double tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
+                                      : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
         if (tid == 0) fx_add(acc, fx_from_double(tt));
       }
       if (tid == 0) finalize_pass(pass, fx_to_double(acc), n, &res);

@@ -394,8 +394,9 @@ def test_psi_r_at_every_tile_shape(P, oracle_mod, n):
         assert rel(got, ref) < TOL, (n, r, got, ref)
 
 
-def test_batch_bit_identical_to_single_runs(P):
-    # plugin_h_batch: one CTA per sample, each result bit-identical to plugin_h on the sample
+def test_batch_matches_single_runs(P, oracle_mod):
+    # plugin_h_batch: one CTA per sample with T = 1024 tiles; each result agrees with plugin_h on
+    # the sample (T = 64 tiles) to fp32 evaluation rounding, and with the oracle at TOL
     rng = np.random.default_rng(11)
     sizes = [2, 3, 64, 65, 128, 300, 1000, 1024, 1500, 2048, 1, 2049, 700]
     samples = []
@@ -414,7 +415,16 @@ def test_batch_bit_identical_to_single_runs(P):
             assert r["status"] == P.PLUGIN_E_INVALID
             continue
         one = P.read_result(P.plugin_h(torch.from_numpy(s).cuda()))
-        assert _same(one, r), (s.size, one, r)
+        if one["status"] != 0:
+            assert r["status"] == one["status"]
+            continue
+        assert r["status"] == 0 and r["sigma"] == one["sigma"] and r["g1"] == one["g1"]  # same Step I
+        for key in ("psi6", "psi4", "h"):
+            assert rel(r[key], one[key]) < TOL, (s.size, key, r[key], one[key])
+        if s.size in (300, 2048):
+            o = oracle_mod.plugin(s)
+            for key in ("psi6_z", "psi4_z", "h"):
+                assert rel(r[key], o[key]) < TOL, (s.size, key, r[key], o[key])
     assert res[-2]["status"] == P.PLUGIN_E_DEGENERATE and res[-1]["status"] == P.PLUGIN_E_NONFINITE
     empty = P.plugin_h_batch(x, torch.zeros(1, dtype=torch.int64, device="cuda"))
     assert empty.numel() == P.RESULT_BYTES
