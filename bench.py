@@ -588,8 +588,10 @@ def run_batch(a):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
     peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
-    # the batch kernel's single T = 1024 tile per pass is a full n x n square (n = 1024)
-    evaluated = count * 2 * n * n
+    # the batch kernel's tiles (T = 256 R; diagonal tiles as full squares): nb (nb + 1) / 2 of T^2
+    T = 256 * int(os.environ.get("PLUGIN_BATCH_R_REPORT", "4"))
+    nbt = -(-n // T)
+    evaluated = count * 2 * (nbt * (nbt + 1) // 2) * min(T, n) ** 2
     res = P.read_results(out, 2)
     line = {"metric": "pairwise K4/K6 evaluations/sec, batches of independent samples", "value": pairs / (ms / 1e3) / 1e9,
             "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,

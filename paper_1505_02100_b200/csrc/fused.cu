@@ -168,7 +168,10 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
 // centred form of psi.cu: a whole sample is 1-3 tiles, ~2^20 pairs per tile, where the small
 // tiles of the latency path would be overhead-bound) and the same finalize.  The tiles differ
 // from plugin_h's, so results agree with it to fp32 evaluation rounding, not bit for bit.
-constexpr int kBatchR = 4, kBatchT = kPsiThreads * kBatchR;
+#ifndef BATCH_R
+#define BATCH_R 4  // rows per thread of the batch tiles (T = 256 R); tuning: 1, 2, 4
+#endif
+constexpr int kBatchR = BATCH_R, kBatchT = kPsiThreads * kBatchR;
 
 __global__ void __launch_bounds__(kPsiThreads, 2)
 plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets, int count, int skip,
