@@ -589,7 +589,7 @@ def run_batch(a):
     f_meas = clocks.get("sm_mhz") or 1965.0
     peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
     # the batch kernel's tiles (T = 256 R; diagonal tiles as full squares): nb (nb + 1) / 2 of T^2
-    T = 256 * int(os.environ.get("PLUGIN_BATCH_R_REPORT", "4"))
+    T = 256 * int(os.environ.get("PLUGIN_BATCH_R_REPORT", "1"))
     nbt = -(-n // T)
     evaluated = count * 2 * (nbt * (nbt + 1) // 2) * min(T, n) ** 2
     res = P.read_results(out, 2)

@@ -164,12 +164,13 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
 
 // Many small samples in one launch (plugin_h_batch): CTA b runs the whole algorithm for sample
 // b (2 <= n_b <= 2048) on its own -- no grid barrier: the prologue above (the same sort and
-// Step I as plugin_h), then each pass over tiles of T = 1024 (R = 4 rows per thread, the
-// centred form of psi.cu: a whole sample is 1-3 tiles, ~2^20 pairs per tile, where the small
-// tiles of the latency path would be overhead-bound) and the same finalize.  The tiles differ
+// Step I as plugin_h), then each pass over tiles of T = 256 BATCH_R (the centred form of psi.cu;
+// at one CTA per sample the T = 64 tiles of the latency path are overhead-bound, and larger
+// tiles waste more on the full-square diagonal tiles: T = 256 measured fastest) and the same
+// finalize.  The tiles differ
 // from plugin_h's, so results agree with it to fp32 evaluation rounding, not bit for bit.
 #ifndef BATCH_R
-#define BATCH_R 4  // rows per thread of the batch tiles (T = 256 R); tuning: 1, 2, 4
+#define BATCH_R 1  // rows per thread of the batch tiles (T = 256 R); A/B: 1 fastest (less full-square waste)
 #endif
 constexpr int kBatchR = BATCH_R, kBatchT = kPsiThreads * kBatchR;
 
