@@ -74,3 +74,16 @@ def test_dpi_errors(P):
     c = torch.full((64,), 2.0, device="cuda")
     assert P.read_dpi_result(P.plugin_dpi(c, 3))["status"] == P.PLUGIN_E_DEGENERATE
     assert math.isnan(P.read_dpi_result(P.plugin_dpi(c, 3))["h"])
+
+
+@pytest.mark.parametrize("stages", [3, 5])
+def test_dpi_at_config3_size(P, oracle_mod, stages):
+    # the higher-order passes (r = 8 .. 12) cancel more (C ~ g^-r): check them at n = 131072
+    # (BASELINE config 3) against the oracle (its 3-5 passes take ~10-20 s on the GPU box)
+    x = inputs.config_data(3)
+    got = P.read_dpi_result(P.plugin_dpi(torch.from_numpy(x).cuda(), stages))
+    ref = oracle_mod.dpi(x, stages)
+    assert got["status"] == 0
+    assert rel(got["h"], ref["h"]) < TOL
+    for j in range(1, stages + 1):
+        assert rel(got["psi_z"][j], ref["psi_z"][j]) < TOL, (j, got["psi_z"][j], ref["psi_z"][j])
