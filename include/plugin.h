@@ -112,6 +112,18 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
 plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int count, plugin_result* d_out,
                              unsigned int flags, void* stream);
 
+/* plugin_h as a CUDA graph, for repeated runs on the same buffers (the launch latency of the
+ * kernel sequence -- or of the one cooperative launch for n <= 2048 -- is paid once at
+ * creation).  plugin_graph_create captures plugin_h_ex(d_x, n, d_out, flags, d_ws, ws_bytes)
+ * with its arguments fixed: the caller keeps d_x, d_out and d_ws alive and may change the
+ * CONTENTS of d_x between launches.  The handle (host memory, owned by the caller) is freed by
+ * plugin_graph_destroy.  plugin_graph_launch runs it on `stream`, asynchronously. */
+typedef struct plugin_graph plugin_graph;
+plugin_status plugin_graph_create(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws,
+                                  size_t ws_bytes, unsigned int flags, plugin_graph** out_graph);
+plugin_status plugin_graph_launch(plugin_graph* graph, void* stream);
+void plugin_graph_destroy(plugin_graph* graph);
+
 /* Same as plugin_h (device result kept in the workspace), then synchronises `stream`,
  * copies the result to *h_out and returns its data status (PLUGIN_OK or one of
  * E_NONFINITE/E_DEGENERATE/E_DOMAIN). */

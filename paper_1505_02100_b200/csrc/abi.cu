@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <new>
 
 #include "common.cuh"
 
@@ -276,6 +277,62 @@ plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int cou
                                static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "batch");
   return PLUGIN_OK;
+}
+
+struct plugin_graph {
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+};
+
+plugin_status plugin_graph_create(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes,
+                                  unsigned int flags, plugin_graph** out_graph) {
+  g_err[0] = 0;
+  if (!out_graph) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  *out_graph = nullptr;
+  cudaStream_t cs;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "graph stream");
+  if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return cuda_fail(e, "begin capture");
+  }
+  plugin_status st = plugin_h_ex(d_x, n, d_out, flags, d_ws, ws_bytes, cs);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(cs, &graph);
+  cudaStreamDestroy(cs);
+  if (st != PLUGIN_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "end capture");
+  cudaGraphExec_t exec;
+  if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(e, "instantiate");
+  }
+  plugin_graph* g = new (std::nothrow) plugin_graph{graph, exec};
+  if (!g) {
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    return fail(PLUGIN_E_INVALID, "out of host memory%s");
+  }
+  *out_graph = g;
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_graph_launch(plugin_graph* g, void* stream) {
+  g_err[0] = 0;
+  if (!g) return fail(PLUGIN_E_INVALID, "null graph%s");
+  cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  return PLUGIN_OK;
+}
+
+void plugin_graph_destroy(plugin_graph* g) {
+  if (!g) return;
+  cudaGraphExecDestroy(g->exec);
+  cudaGraphDestroy(g->graph);
+  delete g;
 }
 
 plugin_status plugin_sort(const float* d_x, int64_t n, float* d_sorted, void* d_ws, size_t ws_bytes, void* stream) {

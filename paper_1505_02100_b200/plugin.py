@@ -75,6 +75,9 @@ def lib():
             "plugin_h_ex": (i32, [P, i64, P, ctypes.c_uint, P, sz, P]),
             "plugin_h_sync": (i32, [P, i64, P, P, sz, P]),
             "plugin_h_batch": (i32, [P, P, i32, P, ctypes.c_uint, P]),
+            "plugin_graph_create": (i32, [P, i64, P, P, sz, ctypes.c_uint, ctypes.POINTER(P)]),
+            "plugin_graph_launch": (i32, [P, P]),
+            "plugin_graph_destroy": (None, [P]),
             "plugin_h_host": (i32, [P, i64, P, P, sz, P]),
             "psi_r": (i32, [P, i64, d, i32, P, P, sz, P]),
             "plugin_step1": (i32, [P, i64, P, P, sz, P]),
@@ -107,6 +110,7 @@ PLUGIN_SKIP_UNDERFLOW = 1
 PLUGIN_MULTI_KERNEL = 2
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_batch",
+            "plugin_graph_create", "plugin_graph_launch", "plugin_graph_destroy",
             "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
             "plugin_shard_tiles", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
@@ -187,6 +191,37 @@ def plugin_h_batch(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | N
     _check(lib().plugin_h_batch(x.data_ptr(), offsets.data_ptr(), count, out.data_ptr(), int(flags),
                                 _stream(stream)))
     return out
+
+
+class PluginGraph:
+    """plugin_h on fixed buffers as a CUDA graph (plugin_graph_create / _launch / _destroy):
+    refill x in place, call launch(), read the result buffer."""
+
+    def __init__(self, x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                 flags: int = 0):
+        self.x = _x(x)
+        n = self.x.numel()
+        self.ws = workspace(n, self.x.device) if ws is None else ws
+        self.out = new_result(self.x.device) if out is None else out
+        h = ctypes.c_void_p()
+        _check(lib().plugin_graph_create(self.x.data_ptr(), n, self.out.data_ptr(), self.ws.data_ptr(),
+                                         self.ws.numel(), int(flags), ctypes.byref(h)))
+        self.handle = h
+
+    def launch(self, stream=None) -> torch.Tensor:
+        _check(lib().plugin_graph_launch(self.handle, _stream(stream)))
+        return self.out
+
+    def close(self):
+        if self.handle:
+            lib().plugin_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def read_results(buf: torch.Tensor, count: int) -> list[dict]:

@@ -428,3 +428,19 @@ def test_batch_matches_single_runs(P, oracle_mod):
     assert res[-2]["status"] == P.PLUGIN_E_DEGENERATE and res[-1]["status"] == P.PLUGIN_E_NONFINITE
     empty = P.plugin_h_batch(x, torch.zeros(1, dtype=torch.int64, device="cuda"))
     assert empty.numel() == P.RESULT_BYTES
+
+
+@pytest.mark.parametrize("n", [1000, 50000])
+def test_graph_api_repeats_plugin_h(P, n):
+    # plugin_graph_*: one capture (the cooperative launch for n <= 2048, the kernel sequence
+    # above), many launches with the sample refilled in place: each result bit-identical to
+    # plugin_h on the same data
+    x = torch.empty(n, device="cuda")
+    g = P.PluginGraph(x)
+    for seed in (1, 2, 3):
+        xs = inputs.mixture(n, 900 + seed)
+        x.copy_(torch.from_numpy(xs))
+        got = P.read_result(g.launch())
+        ref = P.read_result(P.plugin_h(torch.from_numpy(xs).cuda()))
+        assert _same(got, ref), (n, seed)
+    g.close()
