@@ -80,6 +80,11 @@ def main():
             row["graph_default_us"], row["graph_default_min_us"] = med, mn
         except Exception as e:  # report, do not hide: the header claims capturability
             row["graph_default_error"] = repr(e)
+        # the library's own graph API (plugin_graph_create / _launch)
+        pg = P.PluginGraph(x, out=out, ws=ws)
+        med, mn = dev_time(lambda: pg.launch(), a.reps)
+        row["plugin_graph_us"], row["plugin_graph_min_us"] = med, mn
+        pg.close()
         row["h"] = h_default
         row["same_h_all_paths"] = P.read_result(out)["h"] == h_default
         xpin = torch.from_numpy(xh).pin_memory()
