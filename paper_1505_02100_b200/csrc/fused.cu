@@ -210,12 +210,18 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
             ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
           continue;
         const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-        const float cen = PSI_CENTER ? xsm[i0] : 0.f;
+        const bool wide = psi_tile_wide(xsm[i0], xsm[(i0 + T < n ? i0 + T : n) - 1], xsm[j0 + jcount - 1], s);
+        const float cen = (PSI_CENTER && !wide) ? xsm[i0] : 0.f;
         __syncthreads();  // sx of the previous tile consumed
         for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((j0 + q < n) ? xsm[j0 + q] : xpad, cen);
         const double w = (bi == bj) ? 1.0 : 2.0;
-        const double tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
-                                      : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
+        double tt;
+        if (wide)  // see psi_tile_wide
+          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red)
+                           : psi_tile_sum<kBatchR, 4, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red);
+        else
+          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
+                           : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
         if (tid == 0) fx_add(acc, fx_from_double(tt));
       }
       if (tid == 0) finalize_pass(pass, fx_to_double(acc), n, &res);

@@ -77,8 +77,11 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       }
     }
     const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-    // tile centre (R >= 1 tiles, PSI_CENTER): the first row's value; sx holds fl(x_j - cen)
-    const float cen = (R > 0 && PSI_CENTER) ? __ldg(xs + i0) : 0.f;
+    // sorted: rows in [xs[i0], xs[i0 + T - 1]], values in [xs[i0], xs[j0 + jcount - 1]]
+    const bool wide = R > 0 && psi_tile_wide(__ldg(xs + i0), __ldg(xs + (i0 + T < n ? i0 + T : n) - 1),
+                                             __ldg(xs + j0 + jcount - 1), s);
+    // tile centre (R >= 1 tiles, PSI_CENTER, not wide): the first row's value; sx holds fl(x_j - cen)
+    const float cen = (R > 0 && PSI_CENTER && !wide) ? __ldg(xs + i0) : 0.f;
     // stage the tile's j values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
     if (jcount == T) {
       const float4* src = reinterpret_cast<const float4*>(xs + j0);
@@ -97,8 +100,12 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
-    if constexpr (R == 0) tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
-    else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
+    if constexpr (R == 0) {
+      tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+    } else {
+      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
+    }
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
   }

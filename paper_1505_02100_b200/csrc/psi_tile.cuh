@@ -73,11 +73,34 @@ __device__ __forceinline__ u64 hermite_t(u64 t) {
 // CENTER = false: xj, xi are raw sample values, u = (x_j - x_i) s (difference first).
 // CENTER = true (PSI_CENTER): xj = fl(x_j - c) and xi = -fl(fl(x_i - c) s) for a tile centre c
 // (the tile's first row), u = fma(xj, s, xi): one FP32 op instead of two.
-template <int ORDER, bool MASK, bool CENTER = false>
+// CLAMP: t = min(t, kTClamp) first.  Far pairs have e = +0 exactly either way, but without
+// the clamp He_r(t) overflows fp32 to inf once |u| passes ~1600 (r = 12) ... ~2.6e6 (r = 6),
+// and inf * 0 = NaN; with it He_r(t) <= 1024^6 stays finite and the term is exactly 0, so a
+// clamped evaluation is bit-identical to an unclamped one wherever the latter is finite.
+constexpr float kTClamp = 1024.f;  // a <= -0.7213 * 1024 - 1: ex2 -> +0
+// "wide" tiles take the variant psi_tile_sum<..., WIDE = true>: difference first and clamped,
+// inner loop rolled.  A tile is wide if its values span more than kClampSpan bandwidths
+// (otherwise |u| <= span * s and He_12(1000^2) < 1e37: no overflow), or its ROWS span more than
+// kCenterSpan bandwidths (the centred form shifts each row by eps * |x_i - c| * s in u, DESIGN.md
+// §6.7: fine for a dense row block, not for one that holds an outlier).  Both only occur with
+// outliers or a tiny g; none of the BASELINE configurations has such a tile.
+constexpr double kClampSpan = 1000.0;
+constexpr double kCenterSpan = 64.0;
+__device__ __forceinline__ bool psi_tile_wide(float row_lo, float row_hi, float col_hi, float s) {
+  return ((double)row_hi - (double)row_lo) * (double)s > kCenterSpan ||
+         ((double)col_hi - (double)row_lo) * (double)s > kClampSpan;
+}
+
+template <int ORDER, bool MASK, bool CENTER = false, bool CLAMP = false>
 __device__ __forceinline__ void pair2(u64 xj, u64 xi, u64 s2, u64 ph, u64& acc, bool m0 = true, bool m1 = true) {
   const u64 c2 = 0xBF38AA3BBF38AA3Bull;  // {fp32(-log2(e)/2)} x 2 = -0.72134752f
   u64 u = CENTER ? fma2(xj, s2, xi) : mul2(sub2(xj, xi), s2);
   u64 t = mul2(u, u);
+  if (CLAMP) {
+    float t0, t1;
+    upk2(t, t0, t1);
+    t = pk2(fminf(t0, kTClamp), fminf(t1, kTClamp));
+  }
   u64 a = fma2(t, c2, ph);
   float a0, a1;
   upk2(a, a0, a1);
@@ -156,12 +179,15 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
 #endif
 
 // cen: the tile centre when PSI_CENTER (sx then holds fl(x_j - cen)); ignored otherwise
-template <int R, int ORDER, bool LDG>
+// WIDE (psi_tile_wide): difference first (sx holds raw values, cen unused) and pair2's overflow
+// clamp; the inner loop stays rolled there to keep the code small.
+template <int R, int ORDER, bool LDG, bool WIDE = false>
 __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __restrict__ xrows, int64_t n, int64_t i0,
                                                int jcount, float s, float xpad, double w, double* red,
                                                float cen = 0.f) {
   constexpr int CH = PSI_CH;  // j per fp32 chunk (CH/2 per packed lane) before the fp64 flush
-  constexpr bool CEN = PSI_CENTER != 0;
+  constexpr bool CEN = PSI_CENTER != 0 && !WIDE;
+  constexpr bool CLAMP = WIDE;
   const int tid = threadIdx.x;
   u64 xi[R], ph[R], s2[R];
   double drow[R];
@@ -184,12 +210,17 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
     u64 acc[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0ull;
-#pragma unroll kPsiUnroll
+#pragma unroll(CLAMP ? 1 : kPsiUnroll)
     for (int q = 0; q < CH / 4; ++q) {
       const float4 v = sx4[c * (CH / 4) + q];
       const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
+        if (CLAMP) {
+          pair2<ORDER, false, CEN, true>(j01, xi[k], s2[k], ph[k], acc[k]);
+          pair2<ORDER, false, CEN, true>(j23, xi[k], s2[k], ph[k], acc[k]);
+          continue;
+        }
         pair2<ORDER, false, CEN>(j01, xi[k], s2[k], ph[k], acc[k]);
         if (PSI_HYB4 && ORDER == 4 && R == 8 && (k == (q & 7) || k == ((q + 4) & 7)))
           pair2_fma<ORDER, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
@@ -215,8 +246,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
       const u64 j01 = pk2(v.x, v.y), j23 = pk2(v.z, v.w);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        pair2<ORDER, true, CEN>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
-        pair2<ORDER, true, CEN>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
+        pair2<ORDER, true, CEN, CLAMP>(j01, xi[k], s2[k], ph[k], acc[k], j < jcount, j + 1 < jcount);
+        pair2<ORDER, true, CEN, CLAMP>(j23, xi[k], s2[k], ph[k], acc[k], j + 2 < jcount, j + 3 < jcount);
       }
     }
 #pragma unroll
@@ -249,8 +280,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
 // Small tiles for small n (R = 0 in psi_rows_per_thread: n <= kFusedMaxN): T = 64 rows x 64
 // columns, thread tid takes row tid % 64 and the 16 columns 16 (tid / 64) .. + 15, so a pass
 // has 4x more, 16x smaller tiles than at T = 256 and spreads over the SMs (at these sizes the
-// pass is latency-bound).  Same pair arithmetic (pair2), dither and per-thread fp64 flush; the
-// result is valid in thread 0.  Contains __syncthreads().
+// pass is latency-bound).  Same pair arithmetic (pair2, always with the overflow clamp), dither
+// and per-thread fp64 flush; the result is valid in thread 0.  Contains __syncthreads().
 constexpr int kPsiSmallT = 64;
 
 template <int ORDER, bool LDG>
@@ -273,16 +304,16 @@ __device__ __forceinline__ double psi_tile_sum_small(const float* sx, const floa
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float4 t = sx4[q];
-      pair2<ORDER, false>(pk2(t.x, t.y), xi, s2, ph, acc);
-      pair2<ORDER, false>(pk2(t.z, t.w), xi, s2, ph, acc);
+      pair2<ORDER, false, false, true>(pk2(t.x, t.y), xi, s2, ph, acc);
+      pair2<ORDER, false, false, true>(pk2(t.z, t.w), xi, s2, ph, acc);
     }
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float4 t = sx4[q];
       const int j = jq + 4 * q;
-      pair2<ORDER, true>(pk2(t.x, t.y), xi, s2, ph, acc, j < jcount, j + 1 < jcount);
-      pair2<ORDER, true>(pk2(t.z, t.w), xi, s2, ph, acc, j + 2 < jcount, j + 3 < jcount);
+      pair2<ORDER, true, false, true>(pk2(t.x, t.y), xi, s2, ph, acc, j < jcount, j + 1 < jcount);
+      pair2<ORDER, true, false, true>(pk2(t.z, t.w), xi, s2, ph, acc, j + 2 < jcount, j + 3 < jcount);
     }
   }
   float a0, a1;

@@ -180,7 +180,7 @@ def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor 
 def plugin_h_batch(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None, stream=None,
                    flags: int = 0) -> torch.Tensor:
     """Alg. 1 for every sample x[offsets[b]:offsets[b+1]] (2 <= n_b <= 2048), one CTA each
-    (T = 1024 tiles: agrees with plugin_h to fp32 rounding); returns the device buffer of count
+    (T = 256 tiles: agrees with plugin_h to fp32 rounding); returns the device buffer of count
     plugin_result records (read_results decodes it)."""
     x = _x(x)
     if not (isinstance(offsets, torch.Tensor) and offsets.is_cuda and offsets.dtype == torch.int64):

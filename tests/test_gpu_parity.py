@@ -444,3 +444,42 @@ def test_graph_api_repeats_plugin_h(P, n):
         ref = P.read_result(P.plugin_h(torch.from_numpy(xs).cuda()))
         assert _same(got, ref), (n, seed)
     g.close()
+
+
+@pytest.mark.parametrize("n", [2, 1500, 5000])
+@pytest.mark.parametrize("r", [4, 6, 8, 10, 12])
+def test_psi_r_far_pairs_do_not_overflow(P, oracle_mod, n, r):
+    # |u| = |x_i - x_j| / g far beyond the exp underflow: K^(r)(u) = 0, but the fp32 He_r(u^2)
+    # overflows to inf (|u| > ~1600 at r = 12 ... ~4e9 at r = 4) and inf * 0 would be NaN;
+    # the pair evaluation clamps u^2 (psi_tile.cuh kTClamp) on tiles that span that far
+    if n == 2:
+        x, g = np.array([0.0, 1e7], dtype=np.float32), (1e-3 if r == 4 else 1.0)
+    else:
+        rng = np.random.default_rng(40 + n)
+        far = np.array([3e3, -5e3, 1e5, 1e7, -2e4], dtype=np.float32)
+        x = np.concatenate([rng.normal(0, 1, n - far.size).astype(np.float32), far])
+        x = x[rng.permutation(n)]
+        g = 1.0
+    got = P.psi_r(torch.from_numpy(x).cuda(), g, r).item()
+    ref = oracle_mod.psi(oracle_mod.widen(x), g, r)
+    assert math.isfinite(got) and rel(got, ref) < TOL, (n, r, got, ref)
+
+
+@pytest.mark.parametrize("n", [1800, 50000])
+def test_plugin_h_with_outliers(P, oracle_mod, n):
+    # a few points 1e4 sigma out: the tiles holding them span > kCenterSpan bandwidths and take
+    # the difference-first variant (psi_tile_wide); the batch kernel decides the same way
+    rng = np.random.default_rng(77)
+    x = np.concatenate([rng.normal(0, 1, n - 4), [1e4, -2e4, 3e4, 2.5]]).astype(np.float32)
+    x = x[rng.permutation(n)]
+    got = P.plugin_h_sync(torch.from_numpy(x).cuda())
+    ref = oracle_mod.plugin(x)
+    assert got["status"] == 0
+    for key in ("psi6", "psi4", "h"):
+        assert rel(got[key], ref[key]) < TOL, (key, got[key], ref[key])
+    if n <= 2048:
+        xt = torch.from_numpy(x).cuda()
+        offs = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+        b = P.read_results(P.plugin_h_batch(xt, offs), 1)[0]
+        for key in ("psi6", "psi4", "h"):
+            assert rel(b[key], ref[key]) < TOL, (key, b[key], ref[key])
