@@ -274,6 +274,9 @@ static int64_t q32_term_c(const int64_t* c, int64_t d, int64_t rg, int r) {
   const int64_t one = 4294967296LL;
   const int64_t a = d < 0 ? -d : d;
   const int64_t u = oracle_q32_mul(a, rg);
+  /* u > 7 implies t = floor(u^2) > 42, so the term is 0 (reading Q4); testing u first keeps
+   * floor(u*u / 2^32) inside int64 (it wraps for u >= 46341) */
+  if (u > 7 * one) return 0;
   const int64_t t = oracle_q32_mul(u, u);
   if (t > 42 * one) return 0;
   const int64_t e = q32_exp_c(c, -(t >> 1));

@@ -62,6 +62,7 @@ __device__ __forceinline__ long long q32_term(long long d, long long rg) {
   const long long one = 4294967296LL;
   const long long a = d < 0 ? -d : d;
   const long long u = q32_mul(a, rg);
+  if (u > 7 * one) return 0;  // then t > 42 too; and u*u would leave int64 for u >= 46341
   const long long t = q32_mul(u, u);
   if (t > 42 * one) return 0;  // e^{-t/2} below the e^-21 clamp
   const long long e = q32_exp(-(t >> 1));

@@ -97,3 +97,13 @@ def test_table4_accuracy_at_the_papers_sizes(P, oracle_mod, n):
     TABLE4[n] = {"h_ref": ref, "fp32_path": h32, "q32_path": hq, "rel_fp32": abs(h32 - ref) / ref,
                  "rel_q32": abs(hq - ref) / ref}
     assert TABLE4[n]["rel_fp32"] <= 4.2e-6 and TABLE4[n]["rel_q32"] <= 4.2e-6
+
+
+def test_psi_q32_far_pairs_bit_exact(P, oracle_mod):
+    # differences up to 1e5 bandwidths: the far terms are exactly 0 on both sides
+    rng = np.random.default_rng(5)
+    z = np.concatenate([rng.normal(0, 1, 3000), [5e4, -5e4, 2e4]])
+    zq = oracle_mod.q32_encode(z)
+    rg = ONE
+    got = P.psi_r_q32(torch.from_numpy(zq).cuda(), rg, 4)
+    assert got == 2 * oracle_mod.q32_psi_sum(zq, rg, 4) + zq.size * oracle_mod.q32_term(0, rg, 4)

@@ -108,3 +108,14 @@ def test_h_within_the_papers_fixed_point_accuracy(oracle_mod, n):
     assert abs(a["h"] - b["h"]) / b["h"] <= 4.2e-6
     assert abs(a["psi4_z"] - b["psi4_z"]) / b["psi4_z"] <= 2.1e-5
     assert a["psi6_z"] < 0 < a["psi4_z"]
+
+
+@pytest.mark.parametrize("r", [4, 6])
+def test_term_is_zero_far_out(oracle_mod, r):
+    # K^(r)(u) = 0 to all Q32.32 digits for |u| > 7 (reading Q4); u*u leaves int64 at
+    # u >= 46341, which must not wrap into a non-zero term
+    for u in (7.5, 100.0, 46340.0, 46341.0, 46342.0, 70000.0, 2.0 ** 18, 2.0 ** 30):
+        d = int(u * ONE)
+        assert oracle_mod.q32_term(d, ONE, r) == 0, u
+        assert oracle_mod.q32_term(-d, ONE, r) == 0, u
+    assert oracle_mod.q32_term(7 * ONE, ONE, r) == 0  # t = 49 > 42
