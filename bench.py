@@ -122,6 +122,17 @@ def _traffic(n):
     return t["dram_bytes_read_per_launch"] + t["dram_bytes_write_per_launch"]
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_sample(k: int, seconds: float, threads: int = 0):
     """Time the oracle (as it stands) on rows [0, m) of both passes of config k."""
     import numpy as np
@@ -383,6 +394,11 @@ def run_ours(a):
         if not a.no_cpu_baseline and world == 1:
             cb = cpu_oracle_sample(a.config, a.cpu_seconds)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            # also one thread, and the CPU model
+            cb1 = cpu_oracle_sample(a.config, min(3.0, a.cpu_seconds / 4), threads=1)
+            cpu_oracle_sample(a.config, 0.05, threads=cb["cores"])  # restore the OpenMP team size
+            line["cpu_baseline"]["single_thread_value"] = cb1["value"]
+            line["cpu_baseline"]["cpu_model"] = cpu_model()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
