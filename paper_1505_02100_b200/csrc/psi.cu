@@ -124,11 +124,15 @@ int psi_rows_per_thread(int64_t n) {
     if (r == 8 || r == 4 || r == 2 || r == 1 || (r == 0 && n <= kFusedMaxN)) return r;
   }
   if (n <= kFusedMaxN) return 0;  // small tiles (T = 64): latency-bound sizes
-  // largest R in {8,4,2} whose tile count keeps >= ~28 tiles per resident CTA (296 on 148 SMs)
+  // the largest R whose T = 256 R tiles number at least min_tiles[R]: R = 8 needs ~28 tiles per
+  // resident CTA (296 on 148 SMs); the smaller R (3 CTAs per SM) need fewer -- measured sweep
+  // of R = 1, 2, 4 at n = 3000 ... 130000 (profiles/r01ae_tiles_sweep.txt): R = 2 wins from
+  // n ~ 16K (32 blocks), R = 4 from n ~ 65K (64 blocks)
   const int cand[3] = {8, 4, 2};
-  for (int c : cand) {
-    int64_t T = (int64_t)kPsiThreads * c, nb = (n + T - 1) / T;
-    if (nb * (nb + 1) / 2 >= 8192) return c;
+  const int64_t min_blocks[3] = {128, 64, 32};
+  for (int k = 0; k < 3; ++k) {
+    int64_t T = (int64_t)kPsiThreads * cand[k], nb = (n + T - 1) / T;
+    if (nb >= min_blocks[k]) return cand[k];
   }
   return 1;
 }
