@@ -34,7 +34,7 @@ Layout layout(int64_t n) {
   off = align_up(off + sizeof(float) * (size_t)(n > 0 ? n : 1), 256);
   L.tmp = off;
   off = align_up(off + sizeof(unsigned int) * (size_t)(n > 0 ? n : 1), 256);
-  L.sort_blocks = (n + kSortTile - 1) / kSortTile;
+  L.sort_blocks = (n + kSortTileSmall - 1) / kSortTileSmall;  // radix hist capacity (either tile)
   if (L.sort_blocks < 1) L.sort_blocks = 1;
   L.hist = off;
   off = align_up(off + sizeof(unsigned int) * 256 * (size_t)L.sort_blocks, 256);

@@ -20,7 +20,11 @@ constexpr double kMu2 = 1.0;                                    // mu_2(K) = 1
 
 // ---- tiling --------------------------------------------------------------------
 constexpr int kPsiThreads = 256;   // threads per CTA of the psi pass
-constexpr int kSortTile = 4096;    // keys per CTA in the radix sort
+// keys per CTA in the radix sort: 2048 up to kSortTileSwitch keys (more CTAs for mid-size n),
+// 4096 above (fewer, longer scatter CTAs; measured, profiles/r01af_sort_ab.txt)
+constexpr int kSortTileSmall = 2048, kSortTileLarge = 4096;
+constexpr int64_t kSortTileSwitch = 262144;
+inline int sort_tile(int64_t n) { return n <= kSortTileSwitch ? kSortTileSmall : kSortTileLarge; }
 constexpr int kSortThreads = 256;
 constexpr int kStep1Blocks = 592;  // 4 x 148: fixed grid so Step I is deterministic
 // Step I grid for n samples (a function of n only: the reduction tree, hence the result, is fixed)

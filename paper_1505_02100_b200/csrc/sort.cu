@@ -25,14 +25,14 @@ __device__ __forceinline__ unsigned int load_key(const void* src, int64_t i) {
 }
 
 // per-tile histogram of digit (key >> shift) & 255, stored digit-major: hist[d * nb + b]
-template <bool FIRST>
+template <bool FIRST, int TILE>
 __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const void* src, int64_t n, int shift,
                                                                  unsigned int* hist, int64_t nb) {
   __shared__ unsigned int h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile;
-  for (int q = threadIdx.x; q < kSortTile; q += kSortThreads) {
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  for (int q = threadIdx.x; q < TILE; q += kSortThreads) {
     int64_t i = base + q;
     if (i < n) atomicAdd(&h[(load_key<FIRST>(src, i) >> shift) & 255u], 1u);
   }
@@ -68,33 +68,63 @@ __device__ __forceinline__ unsigned int block_excl_scan(unsigned int v, unsigned
   return r;
 }
 
-// exclusive scan of hist (length m) in place, single CTA of 1024 threads, coalesced rounds
+// exclusive scan of hist (length m = 256 nb) in place, single CTA of 1024 threads, ONE block
+// scan: thread t owns the contiguous chunk [t c, t c + c) (c a multiple of 4: uint4 loads, all
+// independent), sums it, takes its offset from the block scan of the 1024 sums and rewrites the
+// chunk.  (A loop of 1024-wide block scans costs one barrier chain per 1024 counters: 64 of
+// them at n = 2^20, ~1 us each.)  hist is 256-byte aligned (workspace layout).
 __global__ void __launch_bounds__(1024) sort_scan_kernel(unsigned int* hist, int64_t m) {
   __shared__ unsigned int wt[33];
-  unsigned int carry = 0;
-  for (int64_t base = 0; base < m; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const unsigned int v = (i < m) ? hist[i] : 0u;
-    unsigned int tot;
-    const unsigned int off = block_excl_scan<1024>(v, wt, tot);
-    if (i < m) hist[i] = carry + off;
-    carry += tot;
+  const int64_t c = ((m + 1023) / 1024 + 3) & ~int64_t(3);
+  const int64_t b = (int64_t)threadIdx.x * c;
+  const int64_t e = (b + c < m) ? b + c : m;
+  const bool vec = (b + c <= m);
+  unsigned int sum = 0;
+  if (vec) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(hist + b);
+#pragma unroll 8
+    for (int64_t q = 0; q < c / 4; ++q) {
+      const uint4 v = h4[q];
+      sum += v.x + v.y + v.z + v.w;
+    }
+  } else {
+    for (int64_t i = b; i < e; ++i) sum += hist[i];
+  }
+  unsigned int tot;
+  unsigned int run = block_excl_scan<1024>(sum, wt, tot);
+  if (vec) {
+    uint4* h4 = reinterpret_cast<uint4*>(hist + b);
+#pragma unroll 4
+    for (int64_t q = 0; q < c / 4; ++q) {
+      uint4 v = h4[q], o;
+      o.x = run; run += v.x;
+      o.y = run; run += v.y;
+      o.z = run; run += v.z;
+      o.w = run; run += v.w;
+      h4[q] = o;
+    }
+  } else {
+    for (int64_t i = b; i < e; ++i) {
+      const unsigned int v = hist[i];
+      hist[i] = run;
+      run += v;
+    }
   }
 }
 
-template <bool FIRST, bool LAST>
+template <bool FIRST, bool LAST, int TILE>
 __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const void* src, int64_t n, int shift,
                                                                     const unsigned int* __restrict__ offs,
                                                                     int64_t nb, void* dst) {
-  constexpr int IPT = kSortTile / kSortThreads;  // 16 keys per thread, blocked arrangement
-  __shared__ unsigned int bufA[kSortTile];
-  __shared__ unsigned int bufB[kSortTile];
+  constexpr int IPT = TILE / kSortThreads;  // keys per thread, blocked arrangement
+  __shared__ unsigned int bufA[TILE];
+  __shared__ unsigned int bufB[TILE];
   __shared__ unsigned int wt[33];
   __shared__ unsigned int dstart[256];
   __shared__ unsigned int dcount[256];
-  const int64_t base = (int64_t)blockIdx.x * kSortTile;
-  const int cnt = (int)((n - base) < kSortTile ? (n - base) : kSortTile);
-  for (int q = threadIdx.x; q < kSortTile; q += kSortThreads)
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  const int cnt = (int)((n - base) < TILE ? (n - base) : TILE);
+  for (int q = threadIdx.x; q < TILE; q += kSortThreads)
     bufA[q] = (q < cnt) ? load_key<FIRST>(src, base + q) : 0xffffffffu;  // pads sort last
   dcount[threadIdx.x] = 0;
   __syncthreads();
@@ -210,8 +240,34 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
 
 // x (float) -> xs (float, ascending).  tmp: n uint32; hist: 256*nb uint32.
 // Passes ping-pong tmp <-> xs (reinterpreted as keys); the last pass writes floats into xs.
+// 4 LSD passes of 8 bits; hist holds 256 * ceil(n / TILE) counters (the workspace sizes it for
+// the smaller tile)
+template <int TILE>
+static cudaError_t radix_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
+                              cudaStream_t s) {
+  const int64_t nb = (n + TILE - 1) / TILE;
+  unsigned int* xk = reinterpret_cast<unsigned int*>(xs);
+  const void* src = x;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    void* dst = (pass & 1) ? (void*)xk : (void*)tmp;   // 0: x->tmp, 1: tmp->xs, 2: xs->tmp, 3: tmp->xs
+    if (pass == 0) sort_hist_kernel<true, TILE><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
+    else sort_hist_kernel<false, TILE><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
+    sort_scan_kernel<<<1, 1024, 0, s>>>(hist, 256 * nb);
+    if (pass == 0)
+      sort_scatter_kernel<true, false, TILE><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    else if (pass == 3)
+      sort_scatter_kernel<false, true, TILE><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    else
+      sort_scatter_kernel<false, false, TILE><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
+    src = dst;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
                         int64_t nb, cudaStream_t s) {
+  (void)nb;  // the workspace's counter capacity: 256 * ceil(n / kSortTileSmall) >= what either tile needs
   static int force_radix = -1;  // PLUGIN_SORT_RADIX=1: always the 4-pass radix sort (testing)
   if (force_radix < 0) {
     const char* e = getenv("PLUGIN_SORT_RADIX");
@@ -233,20 +289,8 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
     }
     return cudaGetLastError();
   }
-  unsigned int* xk = reinterpret_cast<unsigned int*>(xs);
-  const void* src = x;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 8 * pass;
-    void* dst = (pass & 1) ? (void*)xk : (void*)tmp;   // 0: x->tmp, 1: tmp->xs, 2: xs->tmp, 3: tmp->xs
-    if (pass == 0) sort_hist_kernel<true><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
-    else sort_hist_kernel<false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb);
-    sort_scan_kernel<<<1, 1024, 0, s>>>(hist, 256 * nb);
-    if (pass == 0) sort_scatter_kernel<true, false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
-    else if (pass == 3) sort_scatter_kernel<false, true><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
-    else sort_scatter_kernel<false, false><<<(unsigned)nb, kSortThreads, 0, s>>>(src, n, shift, hist, nb, dst);
-    src = dst;
-  }
-  return cudaGetLastError();
+  if (sort_tile(n) == kSortTileSmall) return radix_sort<kSortTileSmall>(x, n, xs, tmp, hist, s);
+  return radix_sort<kSortTileLarge>(x, n, xs, tmp, hist, s);
 }
 
 }  // namespace plg
