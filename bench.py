@@ -33,7 +33,8 @@ sys.path.insert(0, ROOT)
 METRIC = "pairwise K4/K6 evaluations/sec (GPairs/s) and end-to-end h time vs FMA/SFU roofline, 1-8 GPUs"
 UNIT = "GPairs/s"
 MUFU_EX2_PER_CLK_PER_SM = 16      # measured: tools/probe/mufu_probe.cu (profiles/r01_mufu_probe.jsonl)
-KERNELS_PER_STEP = 20             # init_result, step1, 4 x (hist, scan, scatter), 2 x (psi, export, finalize)
+KERNELS_PER_STEP = 20             # distributed API: init_result, step1, 4 x (hist, scan, scatter), 2 x (psi, export, finalize)
+KERNELS_PER_PLUGIN_H = 16         # plugin_h, n > 2048: init_result, 4 x 3 sort, step1, 2 x psi (finalize in its last CTA)
 
 
 def _args():
@@ -259,7 +260,7 @@ def run_skip(a):
             "roofline": {"bound": "alu", "achieved": (ev6 + ev4) / (ms / 1e3) / 1e9, "peak": peak, "unit": UNIT,
                          "frac": (ev6 + ev4) / (ms / 1e3) / 1e9 / peak, "traffic": None,
                          "kernel": "whole step over evaluated pairs (includes sort/Step I)"},
-            "h": res["h"], "status": res["status"], "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * a.steps}
+            "h": res["h"], "status": res["status"], "clocks": clocks, "gpu_launches": KERNELS_PER_PLUGIN_H * a.steps}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -143,14 +143,14 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
   }
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
   const int64_t tiles = psi_tiles(n);
-  if ((e = launch_psi(w.xs, n, 6, skip, 0.0, &d_out->g1, &d_out->status, w.ctrl, 0, 0, tiles, s)) != cudaSuccess)
+  // each pass finalises itself in its last CTA (Steps V / VII; PsiFin)
+  PsiFin f6, f4;
+  f6.what = 0, f6.out = d_out, f6.r = 6;
+  f4.what = 1, f4.out = d_out, f4.r = 4;
+  if ((e = launch_psi(w.xs, n, 6, skip, 0.0, &d_out->g1, &d_out->status, w.ctrl, 0, 0, tiles, s, f6)) != cudaSuccess)
     return cuda_fail(e, "psi6");
-  if ((e = launch_finalize(0, w.ctrl, 0, nullptr, d_out, n, 0.0, 6, nullptr, nullptr, s)) != cudaSuccess)
-    return cuda_fail(e, "finalize psi6");
-  if ((e = launch_psi(w.xs, n, 4, skip, 0.0, &d_out->g2, &d_out->status, w.ctrl, 1, 0, tiles, s)) != cudaSuccess)
+  if ((e = launch_psi(w.xs, n, 4, skip, 0.0, &d_out->g2, &d_out->status, w.ctrl, 1, 0, tiles, s, f4)) != cudaSuccess)
     return cuda_fail(e, "psi4");
-  if ((e = launch_finalize(1, w.ctrl, 1, nullptr, d_out, n, 0.0, 4, nullptr, nullptr, s)) != cudaSuccess)
-    return cuda_fail(e, "finalize psi4");
   return PLUGIN_OK;
 }
 
@@ -210,10 +210,10 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
   // Step I reduction only for its non-finite flag (a NaN/Inf sample makes Psi NaN)
   plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
-  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_tiles(n), s)) != cudaSuccess)
+  PsiFin fin;  // Psi_r(g) written by the pass's last CTA
+  fin.what = 2, fin.g = g, fin.r = r, fin.d_psi = d_psi;
+  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_tiles(n), s, fin)) != cudaSuccess)
     return cuda_fail(e, "psi");
-  if ((e = launch_finalize(2, w.ctrl, 1, nullptr, nullptr, n, g, r, d_psi, nullptr, s)) != cudaSuccess)
-    return cuda_fail(e, "finalize");
   return PLUGIN_OK;
 }
 

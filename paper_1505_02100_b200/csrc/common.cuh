@@ -62,7 +62,8 @@ struct Ctrl {                       // zeroed at the start of every API call
   unsigned long long tile_counter[2];  // dynamic tile scheduler per slot (64-bit: n^2 tiles can pass 2^32)
   unsigned int step1_done;          // last-block-done counter of Step I
   int nonfinite;                    // set if any X is NaN/Inf
-  unsigned int pad[56];
+  unsigned int psi_done[2];         // last-CTA-done counters of the psi passes (PsiFin)
+  unsigned int pad[54];
 };
 static_assert(sizeof(Ctrl) <= 512, "ctrl block");
 
@@ -82,9 +83,18 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
 // One pass of Steps IV/VI (or Psi_r for any even r <= 12) over tiles [tile_begin, tile_end):
 // g from *g_dev (a device bandwidth; the pass is skipped unless *status_dev == PLUGIN_OK) or,
 // if g_dev is null, g_host.  skip != 0: skip tiles whose terms are all exactly 0 (NEXT 4).
+// The pass's epilogue, run by its last CTA to finish (saves the finalize launch): what = -1
+// none, 0 / 1 = Steps V / VII of Alg. 1 into *out, 2 = Psi_r(g) into *d_psi (as finalize_kernel).
+struct PsiFin {
+  int what = -1;
+  plugin_result* out = nullptr;
+  double g = 0.0;
+  int r = 0;
+  double* d_psi = nullptr;
+};
 cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_host, const double* g_dev,
                        const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end,
-                       cudaStream_t s);
+                       cudaStream_t s, PsiFin fin = PsiFin());
 // |u| beyond which every fp32 term of a pass is exactly zero (psi.cu, fused.cu)
 constexpr double kSkipU = 13.25;
 // what: 0 = plugin r=6 finalize, 1 = plugin r=4 finalize, 2 = psi_r -> d_psi, 3 = export limbs

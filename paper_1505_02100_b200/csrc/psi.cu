@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "psi_tile.cuh"
+#include "steps.cuh"
 
 namespace plg {
 
@@ -38,7 +39,7 @@ struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R == 0 ? 4 : 3); };
 template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
-           const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end) {
+           const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, PsiFin fin) {
   constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
@@ -109,13 +110,30 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
   }
+  unsigned long long* g_lo = &ctrl->acc[slot].lo;
+  unsigned long long* g_hi = reinterpret_cast<unsigned long long*>(&ctrl->acc[slot].hi);
   if (tid == 0 && (cta_acc.lo != 0ull || cta_acc.hi != 0ll)) {
-    unsigned long long* g_lo = &ctrl->acc[slot].lo;
-    unsigned long long* g_hi = reinterpret_cast<unsigned long long*>(&ctrl->acc[slot].hi);
     unsigned long long old = atomicAdd(g_lo, cta_acc.lo);
     unsigned long long carry = (old + cta_acc.lo < old) ? 1ull : 0ull;
     atomicAdd(g_hi, (unsigned long long)cta_acc.hi + carry);
   }
+  if (fin.what < 0) return;
+  // the last CTA to finish runs the pass's epilogue (threadfence reduction pattern); it also
+  // resets the slot for a later pass on the same workspace
+  __shared__ bool last;
+  if (tid == 0) {
+    __threadfence();
+    last = (atomicAdd(&ctrl->psi_done[slot], 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  Fx128 total;
+  total.lo = atomicExch(g_lo, 0ull);
+  total.hi = (long long)atomicExch(g_hi, 0ull);
+  ctrl->tile_counter[slot] = 0ull;
+  ctrl->psi_done[slot] = 0u;
+  finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
 }
 
 int psi_rows_per_thread(int64_t n) {
@@ -139,7 +157,8 @@ int psi_rows_per_thread(int64_t n) {
 
 template <int R, int ORDER>
 static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, const double* g_dev,
-                            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tb, int64_t te, cudaStream_t s) {
+                            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tb, int64_t te, cudaStream_t s,
+                            PsiFin fin) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 0, occ = 0;
@@ -151,17 +170,20 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   int64_t tiles = te - tb;
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;
-  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te);
+  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, fin);
   return cudaGetLastError();
 }
 
 cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_host, const double* g_dev,
                        const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end,
-                       cudaStream_t s) {
+                       cudaStream_t s, PsiFin fin) {
   const int R = psi_rows_per_thread(n);
-  if (tile_end <= tile_begin) return cudaSuccess;
+  if (tile_end <= tile_begin)  // no tiles: the epilogue still runs (on a zero total)
+    return fin.what >= 0 ? launch_finalize(fin.what, ctrl, slot, nullptr, fin.out, n, fin.g, fin.r, fin.d_psi,
+                                           nullptr, s)
+                         : cudaSuccess;
 #define PLG_ORDER(RR, OO)                                                                                  \
-  if (r == OO) return launch_t<RR, OO>(xs, n, skip, g_host, g_dev, status_dev, ctrl, slot, tile_begin, tile_end, s);
+  if (r == OO) return launch_t<RR, OO>(xs, n, skip, g_host, g_dev, status_dev, ctrl, slot, tile_begin, tile_end, s, fin);
 #define PLG_CASE(RR)                                                                                       \
   if (R == RR) {                                                                                           \
     PLG_ORDER(RR, 6) PLG_ORDER(RR, 4) PLG_ORDER(RR, 0) PLG_ORDER(RR, 2) PLG_ORDER(RR, 8) PLG_ORDER(RR, 10) \

@@ -84,15 +84,7 @@ __global__ void finalize_kernel(int what, Ctrl* ctrl, int slot, const plugin_fx1
     d_limbs->limb[3] = acc.hi >> 32;
     return;
   }
-  const double S = fx_to_double(acc);  // = sum_i sum_j K^(r)(u_ij) / phi(0)
-  const double nd = (double)n;
-  if (what == 2) {  // Psi_r(g) in data units (Step IV/VI form, g given)
-    const double g = g_host;
-    *d_psi = (ctrl && ctrl->nonfinite) ? __longlong_as_double(0x7ff8000000000000LL)
-                                       : kInvSqrt2Pi * S / (nd * nd * ipow(g, r + 1));
-    return;
-  }
-  finalize_pass(what, S, n, out);
+  finalize_total(what, acc, ctrl && ctrl->nonfinite, out, n, g_host, r, d_psi);
 }
 
 cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* total, plugin_result* out,

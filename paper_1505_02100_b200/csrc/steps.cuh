@@ -117,6 +117,20 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
   }
 }
 
+// A pass's epilogue from its fixed-point total (finalize_kernel, and the last CTA of psi_kernel):
+// what = 0 / 1: finalize_pass; 2: Psi_r(g) = phi(0) S / (n^2 g^(r+1)) in data units into *d_psi
+// (NaN if the sample had a non-finite value).  One thread.
+__device__ __forceinline__ void finalize_total(int what, Fx128 acc, bool nonfinite, plugin_result* out, int64_t n,
+                                               double g, int r, double* d_psi) {
+  const double S = fx_to_double(acc);  // = sum_i sum_j K^(r)(u_ij) / phi(0)
+  const double nd = (double)n;
+  if (what == 2) {
+    *d_psi = nonfinite ? __longlong_as_double(0x7ff8000000000000LL) : kInvSqrt2Pi * S / (nd * nd * ipow(g, r + 1));
+    return;
+  }
+  finalize_pass(what, S, n, out);
+}
+
 __device__ __forceinline__ void init_result(plugin_result* out, int64_t n) {
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   out->status = PLUGIN_OK;
