@@ -33,8 +33,8 @@ sys.path.insert(0, ROOT)
 METRIC = "pairwise K4/K6 evaluations/sec (GPairs/s) and end-to-end h time vs FMA/SFU roofline, 1-8 GPUs"
 UNIT = "GPairs/s"
 MUFU_EX2_PER_CLK_PER_SM = 16      # measured: tools/probe/mufu_probe.cu (profiles/r01_mufu_probe.jsonl)
-KERNELS_PER_STEP = 20             # distributed API: init_result, step1, 4 x (hist, scan, scatter), 2 x (psi, export, finalize)
-KERNELS_PER_PLUGIN_H = 16         # plugin_h, n > 2048: init_result, 4 x 3 sort, step1, 2 x psi (finalize in its last CTA)
+KERNELS_PER_STEP = 19             # distributed API: 4 x (hist, scan, scatter), step1, 2 x (psi, export, finalize)
+KERNELS_PER_PLUGIN_H = 15         # plugin_h, n > 2048: 4 x 3 sort, step1, 2 x psi (finalize in its last CTA)
 
 
 def _args():

@@ -79,7 +79,7 @@ static plugin_status check_n(int64_t n, int64_t nmin) {
 static plugin_status run_step1(const float* d_x, int64_t n, plugin_result* d_out, WS& w, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
   if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
-  if ((e = launch_init_result(d_out, n, s)) != cudaSuccess) return cuda_fail(e, "init_result");
+  // (step1_kernel's last block NaN-fills d_out before writing Steps I-III)
   // sort first: Step I then reads the sorted copy, so every result is a function of the
   // multiset of X only (bit-identical under any permutation of the input)
   if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");

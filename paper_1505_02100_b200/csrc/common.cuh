@@ -101,7 +101,6 @@ constexpr double kSkipU = 13.25;
 cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* total, plugin_result* out,
                             int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
                             cudaStream_t s);
-cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s);
 // the whole of Alg. 1 in one cooperative launch for n <= kFusedMaxN (fused.cu); parts holds
 // 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
 constexpr int kFusedMaxGrid = 1024;

@@ -8,10 +8,8 @@
 
 namespace plg {
 
-__global__ void init_result_kernel(plugin_result* out, int64_t n) { init_result(out, n); }
-
-// Step I over a fixed grid (bit-reproducible; see steps.cuh), with the Steps II-III
-// epilogue in the last block to finish.
+// Step I over a fixed grid (bit-reproducible; see steps.cuh), with the result record's
+// initialisation and the Steps II-III epilogue in the last block to finish.
 __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x, int64_t n, Ctrl* ctrl,
                                                     double* __restrict__ partials, plugin_result* out) {
   __shared__ double sh1[8], sh2[8];
@@ -35,12 +33,8 @@ __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x,
   // last block, warp 0: fixed-order sum of the per-block partials
   step1_total<true>(partials, gridDim.x, a, q);
   if (threadIdx.x != 0) return;
+  init_result(out, n);  // NaN-fill the record first (no separate launch): later steps fill it in
   step1_epilogue(a, q, n, K, atomicAdd(&ctrl->nonfinite, 0) != 0, out);
-}
-
-cudaError_t launch_init_result(plugin_result* out, int64_t n, cudaStream_t s) {
-  init_result_kernel<<<1, 1, 0, s>>>(out, n);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials, plugin_result* out,
