@@ -174,6 +174,13 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
 #endif
 constexpr int kBatchR = BATCH_R, kBatchT = kPsiThreads * kBatchR;
 
+// the rare wide tiles of the batch kernel (difference first, clamped), not inlined
+__device__ __noinline__ double batch_wide_tile(int pass, const float* sx, const float* xsm, int64_t n, int64_t i0,
+                                               int jcount, float s, float xpad, double w, double* red) {
+  return (pass == 0) ? psi_tile_sum<kBatchR, 6, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red)
+                     : psi_tile_sum<kBatchR, 4, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red);
+}
+
 __global__ void __launch_bounds__(kPsiThreads, 2)
 plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets, int count, int skip,
                     plugin_result* __restrict__ out) {
@@ -216,9 +223,8 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
         for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((j0 + q < n) ? xsm[j0 + q] : xpad, cen);
         const double w = (bi == bj) ? 1.0 : 2.0;
         double tt;
-        if (wide)  // see psi_tile_wide
-          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red)
-                           : psi_tile_sum<kBatchR, 4, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red);
+        if (wide)  // see psi_tile_wide; out of line so the common path keeps its code and registers
+          tt = batch_wide_tile(pass, sx, xsm, n, i0, jcount, s, xpad, w, red);
         else
           tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
                            : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
