@@ -533,12 +533,12 @@ def run_variant(a):
         ws = torch.empty(P.lib().plugin_q32_workspace_bytes(n) + 256, dtype=torch.uint8, device=dev)
         ws = ws[(-ws.data_ptr()) % 256:][:P.lib().plugin_q32_workspace_bytes(n)]
         step = lambda: P.plugin_h_q32(x, out=out, ws=ws)  # noqa: E731
-        passes, launches = 2, 20
+        passes, launches = 2, 19    # 12 radix sort, Step I, encode, rg1, 2 x (pass, finalize)
     else:
         out = torch.empty(P.DPI_RESULT_BYTES, dtype=torch.uint8, device=dev)
         ws = P.workspace(n, dev)
         step = lambda: P.plugin_dpi(x, a.stages, out=out, ws=ws)  # noqa: E731
-        passes, launches = a.stages, 15 + 2 * a.stages
+        passes, launches = a.stages, 14 + 2 * a.stages  # 12 radix sort, Step I, init, l x (pass, finalize)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(a.warmup):
@@ -566,6 +566,18 @@ def run_variant(a):
             "dtype": "q32.32 (int64)" if a.workload == "q32" else "f32", "data": "synthetic",
             "config": {"workload": f"cfg{a.config} n={n}: {what}", "pairs_per_step": pairs},
             "h": res["h"], "status": res["status"], "clocks": clocks, "gpu_launches": launches * a.steps}
+    if a.workload == "dpi":
+        # per pass r: min(16 MUFU.EX2, 128 / (4 + r/2) FP32 lane-ops) pairs/clk/SM (centred form:
+        # u, t, a, r/2 Horner steps in t, the accumulate); the step's bound is their harmonic mix
+        rs = [2 * j + 2 for j in range(a.stages, 0, -1)]
+        per_clk = len(rs) / sum(1.0 / min(16.0, 128.0 / (4 + r // 2)) for r in rs)
+        mhz = clocks.get("sm_mhz") or 1965.0
+        peak = per_clk * 148 * mhz * 1e6 / 1e9
+        line["roofline"] = {"bound": "alu", "achieved": line["value"], "peak": peak, "unit": UNIT,
+                            "frac": line["value"] / peak, "traffic": None,
+                            "kernel": "whole step (sort, Step I, the l pair passes)",
+                            "peak_basis": f"{per_clk:.2f} pairs/clk/SM (passes r = {rs}: min(16 MUFU, 128/(4 + r/2) FMA))"
+                                          f" x 148 SMs x {mhz:.0f} MHz"}
     print(json.dumps(line), flush=True)
     return 0
 
