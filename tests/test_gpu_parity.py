@@ -483,3 +483,22 @@ def test_plugin_h_with_outliers(P, oracle_mod, n):
         b = P.read_results(P.plugin_h_batch(xt, offs), 1)[0]
         for key in ("psi6", "psi4", "h"):
             assert rel(b[key], ref[key]) < TOL, (key, b[key], ref[key])
+
+
+@pytest.mark.parametrize("n", [5000, 40000])
+def test_data_errors_multi_kernel(P, n):
+    # n > 2048: the multi-kernel sequence, where Step I's last block NaN-fills the record and each
+    # pass finalises itself in its last CTA (or skips on a failed status)
+    x = torch.from_numpy(inputs.normal(n, 5)).cuda()
+    x[n // 3] = float("nan")
+    r = P.plugin_h_sync(x)
+    assert r["status"] == P.PLUGIN_E_NONFINITE
+    assert all(math.isnan(r[k]) for k in ("sigma", "g1", "psi6", "g2", "psi4", "h"))
+    x[n // 3] = float("inf")
+    assert math.isnan(P.psi_r(x, 0.5, 6).item())
+    g = P.PluginGraph(x)
+    assert P.read_result(g.launch())["status"] == P.PLUGIN_E_NONFINITE
+    x[n // 3] = 0.25  # the same buffers, now valid: the graph's next launch succeeds
+    ok = P.read_result(g.launch())
+    assert ok["status"] == 0 and ok["h"] == P.plugin_h_sync(x)["h"]
+    g.close()
