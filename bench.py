@@ -111,14 +111,14 @@ class ClockSampler:
                 "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
 
 
-def _traffic(n):
-    """DRAM bytes per psi launch from the committed ncu --set full capture (same n only)."""
+def _traffic(n, name="psi_traffic.json", m=None):
+    """DRAM bytes per launch of a kernel from its committed ncu --set full capture (same sizes only)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "psi_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             t = json.load(f)
     except OSError:
         return None
-    if t.get("n") != n:
+    if t.get("n") != n or (m is not None and t.get("m") != m):
         return None
     return t["dram_bytes_read_per_launch"] + t["dram_bytes_write_per_launch"]
 
@@ -501,7 +501,9 @@ def run_kde(a):
                        "terms_visited": visited, "terms_effective": n * m,
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GTerms/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "kde_kernel",
+                         "frac": achieved / peak,
+                         "traffic": None if mufu_only else _traffic(n, "kde_traffic.json", m),
+                         "kernel": "kde_kernel",
                          "kernel_ms": k_ms, "prepare_ms": ms - k_ms,
                          "peak_basis": (f"{per_clk:.2f} terms/clk/SM x {sms} SMs x {f_meas:.0f} MHz ("
                                         + ("MUFU.EX2-bound, 1 ex2 per visited term" if mufu_only else
