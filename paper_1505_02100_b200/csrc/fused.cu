@@ -181,7 +181,7 @@ __device__ __noinline__ double batch_wide_tile(int pass, const float* sx, const 
                      : psi_tile_sum<kBatchR, 4, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red);
 }
 
-__global__ void __launch_bounds__(kPsiThreads, 2)
+__global__ void __launch_bounds__(kPsiThreads, 3)
 plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets, int count, int skip,
                     plugin_result* __restrict__ out) {
   extern __shared__ __align__(16) float xsm[];  // 2048 sample + 2048 sort scratch (reused as the j tile)
