@@ -24,6 +24,9 @@
 // fp32 accumulators hold 32 terms per lane (64 per row, PSI_CH), then go to per-row fp64; each tile's fp64
 // total is added as a 128-bit fixed-point integer, so the result does not depend on
 // tile scheduling, grid size or GPU count.
+// Wide tiles (rows spanning > 64 bandwidths, or values > 1000: outliers, tiny g) run difference
+// first with u^2 clamped so He_r cannot overflow (psi_tile_wide).  With a
+// PsiFin, the pass's last CTA runs its epilogue (Steps V / VII or Psi_r) instead of a launch.
 #include <cstdlib>
 
 #include "common.cuh"
