@@ -383,10 +383,11 @@ def test_sort_is_exact(P, n):
     assert np.array_equal(got.view(np.uint32), _key_sorted(x).view(np.uint32))
 
 
-@pytest.mark.parametrize("n", [65023, 70001, 130047])
+@pytest.mark.parametrize("n", [15872, 15873, 20001, 64512, 64513, 70001, 130047])
 def test_psi_r_at_every_tile_shape(P, oracle_mod, n):
-    # the tile edge T = 256 R switches with n (R = 1 below 65024, 2 up to 130047, then 4, 8):
-    # the R = 2 shape and both switch points against the oracle (a few 1e9 pairs, seconds)
+    # the tile edge T = 256 R switches with n (psi_rows_per_thread: R = 1 up to 15872, 2 up to
+    # 64512, 4 up to 260096, then 8): both sides of each switch and ragged R = 2 / R = 4 shapes
+    # against the oracle (up to a few 1e9 pairs, seconds)
     x = inputs.mixture(n, 77)
     for r, g in ((6, 0.4), (4, 0.15)):
         got = P.psi_r(torch.from_numpy(x).cuda(), g, r).item()
