@@ -40,15 +40,20 @@ def cpu_model():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("configs", nargs="+", type=int)
+    ap.add_argument("configs", nargs="+", help="BASELINE config numbers 1..5, or a rounded variant of inputs.ROUNDED (e.g. 4r)")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--ckpt-root", default=os.path.join(ROOT, "tests", "golden", "checkpoints"))
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "tests", "golden"))
     a = ap.parse_args()
     for k in a.configs:
-        x = inputs.config_data(k)
-        sha = inputs.sha256_f32(x)
-        assert sha == inputs.SHA256[k], f"cfg{k} input hash mismatch"
+        if k in inputs.ROUNDED:
+            x = inputs.rounded_data(k)
+            sha = inputs.sha256_f32(x)
+        else:
+            k = int(k)
+            x = inputs.config_data(k)
+            sha = inputs.sha256_f32(x)
+            assert sha == inputs.SHA256[k], f"cfg{k} input hash mismatch"
         ck = os.path.join(a.ckpt_root, f"cfg{k}")
         os.makedirs(ck, exist_ok=True)
         t0 = time.time()

@@ -81,14 +81,33 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       }
     }
     const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-    // sorted: rows in [xs[i0], xs[i0 + T - 1]], values in [xs[i0], xs[j0 + jcount - 1]]
-    const bool wide = R > 0 && psi_tile_wide(__ldg(xs + i0), __ldg(xs + (i0 + T < n ? i0 + T : n) - 1),
-                                             __ldg(xs + j0 + jcount - 1), s);
-    // tile centre (R >= 1 tiles, PSI_CENTER, not wide): the first row's value; sx holds fl(x_j - cen)
-    const float cen = (R > 0 && PSI_CENTER && !wide) ? __ldg(xs + i0) : 0.f;
-    // stage the tile's j values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
-    if (jcount == T) {
-      const float4* src = reinterpret_cast<const float4*>(xs + j0);
+    // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jcount - 1]]
+    // (off-diagonal row blocks are full: only the last block can be ragged, and it is diagonal)
+    int64_t ir = i0, is = j0;  // register-side block, staged block
+    int scount = jcount;
+    float cen = 0.f;
+    bool wide = false;
+    if constexpr (R > 0) {
+      const float a = __ldg(xs + i0), b = __ldg(xs + (i0 + T < n ? i0 + T : n) - 1);
+      const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jcount - 1);
+      bool swap = false;
+      const float c = psi_tile_centre(a, b, p, q, bi == bj, swap);
+      wide = swap ? psi_tile_wide(p, q, a, q, s) : psi_tile_wide(a, b, a, q, s);
+      if (wide) {
+        swap = false;  // difference first: raw values, rows in registers
+      } else if (PSI_CENTER) {
+        cen = c;  // sx holds fl(x_j - cen), exact (psi_tile_centre)
+      }
+      if (swap) {  // the (full) row block is staged, the column block goes to registers
+        ir = j0;
+        is = i0;
+        scount = T;
+      }
+    }
+    // stage the tile's staged-block values: float4 loads (xs is 256-byte aligned, block starts are
+    // multiples of T)
+    if (scount == T) {
+      const float4* src = reinterpret_cast<const float4*>(xs + is);
       float4* dst = reinterpret_cast<float4*>(sx);
       // T / 4 float4 per tile: one per thread for T >= 1024, the first T / 4 threads otherwise
       for (int q = tid; q < T / 4; q += kPsiThreads) {
@@ -100,15 +119,15 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
         dst[q] = v;
       }
     } else {
-      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + j0 + q) : xpad, cen);
+      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < scount) ? __ldg(xs + is + q) : xpad, cen);
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
     if constexpr (R == 0) {
       tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
     } else {
-      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
-      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
+      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, ir, scount, s, xpad, w, red);
+      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, ir, scount, s, xpad, w, red, cen);
     }
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse

@@ -21,16 +21,37 @@ constexpr int kPsiUnroll = PSI_UNROLL;
 // packed constants {v, v}
 #define PK(v) ((((u64)__float_as_uint(v)) << 32) | (u64)__float_as_uint(v))
 
-// per-row dither: phase p_i in (-2, -1] (exact fp32, 24 random bits) and scale offset k_i in [-7, 7]
+// per-row dither: phase p_i in (-2, -1] (exact fp32, 24 random bits) and scale offset k_i
 __device__ __forceinline__ unsigned int row_hash(int64_t i) { return (unsigned int)i * 2654435769u; }
 __device__ __forceinline__ float row_phase(int64_t i) {
   return -1.0f - (float)(row_hash(i) >> 8) * (1.0f / 16777216.0f);
 }
-__device__ __forceinline__ int row_scale_offset(int64_t i) {
-  unsigned int h = ((unsigned int)i * 0x85EBCA6Bu) ^ 0x9E3779B9u;
+// Antithetic scale dither: s_i = s + k_i ulp(s) with k_i uniform in [-A, A]
+// per row pair and k_(2m+1) = -k_(2m), A = scale_dither_amp(n) = min(n / 16, 128).  The dither
+// spreads the fp32 rounding of u, t, a and P(t) over 2A + 1 scales, so the repeated differences of
+// a discretised sample do not all round the same way; the dilation it applies to each row
+// (<= A ulp <= 7.7e-6 relative) cancels to first order between the two rows of a pair (adjacent
+// in sorted order: equal or nearly equal values), leaving a second-order effect ~ (A ulp)^2.  The
+// cancellation needs neighbouring rows closer than a bandwidth, hence the smaller A at small n.
+constexpr int kScaleDither = 128;
+__host__ __device__ __forceinline__ int scale_dither_amp(int64_t n) {
+  return n >= 16 * kScaleDither ? kScaleDither : (int)(n >> 4);
+}
+__device__ __forceinline__ int row_scale_offset(int64_t i, int amp) {
+  unsigned int h = ((unsigned int)(i >> 1) * 0x85EBCA6Bu) ^ 0x9E3779B9u;
   h ^= h >> 15;
   h *= 0x2C1B3C6Du;
-  return (int)(((h >> 16) * 15u) >> 16) - 7;
+  h ^= h >> 13;
+  const int k = (int)(h % (unsigned int)(2 * amp + 1)) - amp;
+  return (i & 1) ? -k : k;
+}
+// s_i = s + k_i ulp(s), exactly (|k_i| << 2^23): symmetric in k_i also when s - |k_i| ulp(s) falls
+// below a power of two (adding k_i to the bit pattern would step by ulp(s)/2 there, a one-sided
+// dilation: measured -1e-5 on psi at s = 1)
+__device__ __forceinline__ float dithered_scale(float s, int64_t i, int64_t n) {
+  const unsigned int e = __float_as_uint(s) & 0x7f800000u;
+  const float ulp = e > (23u << 23) ? __uint_as_float(e - (23u << 23)) : 0.f;  // no dither for s < 2^-103
+  return __fmaf_rn((float)row_scale_offset(i, scale_dither_amp(n)), ulp, s);
 }
 
 // He_r(u) for even r as a polynomial in t = u^2 by Horner, monic, exact integer coefficients
@@ -72,7 +93,7 @@ __device__ __forceinline__ u64 hermite_t(u64 t) {
 
 // CENTER = false: xj, xi are raw sample values, u = (x_j - x_i) s (difference first).
 // CENTER = true (PSI_CENTER): xj = fl(x_j - c) and xi = -fl(fl(x_i - c) s) for a tile centre c
-// (the tile's first row), u = fma(xj, s, xi): one FP32 op instead of two.
+// (psi_tile_centre), u = fma(xj, s, xi): one FP32 op instead of two.
 // CLAMP: t = min(t, kTClamp) first.  Far pairs have e = +0 exactly either way, but without
 // the clamp He_r(t) overflows fp32 to inf once |u| passes ~1600 (r = 12) ... ~2.6e6 (r = 6),
 // and inf * 0 = NaN; with it He_r(t) <= 1024^6 stays finite and the term is exactly 0, so a
@@ -80,15 +101,47 @@ __device__ __forceinline__ u64 hermite_t(u64 t) {
 constexpr float kTClamp = 1024.f;  // a <= -0.7213 * 1024 - 1: ex2 -> +0
 // "wide" tiles take the variant psi_tile_sum<..., WIDE = true>: difference first and clamped,
 // inner loop rolled.  A tile is wide if its values span more than kClampSpan bandwidths
-// (otherwise |u| <= span * s and He_12(1000^2) < 1e37: no overflow), or its ROWS span more than
-// kCenterSpan bandwidths (the centred form shifts each row by eps * |x_i - c| * s in u, DESIGN.md
-// §6.7: fine for a dense row block, not for one that holds an outlier).  Both only occur with
-// outliers or a tiny g; none of the BASELINE configurations has such a tile.
+// (otherwise |u| <= span * s and He_12(1000^2) < 1e37: no overflow), or its register-side block
+// spans more than kCenterSpan bandwidths (the centred form shifts each row by eps * |x_i - c| * s
+// in u: fine for a dense block, not for one that holds an outlier).  Both only
+// occur with outliers or a tiny g; none of the BASELINE configurations has such a tile.
 constexpr double kClampSpan = 1000.0;
 constexpr double kCenterSpan = 64.0;
-__device__ __forceinline__ bool psi_tile_wide(float row_lo, float row_hi, float col_hi, float s) {
-  return ((double)row_hi - (double)row_lo) * (double)s > kCenterSpan ||
-         ((double)col_hi - (double)row_lo) * (double)s > kClampSpan;
+// reg_lo/reg_hi: the register-side (row) block's values; lo/hi: the smallest and largest value of
+// the tile
+__device__ __forceinline__ bool psi_tile_wide(float reg_lo, float reg_hi, float lo, float hi, float s) {
+  return ((double)reg_hi - (double)reg_lo) * (double)s > kCenterSpan || ((double)hi - (double)lo) * (double)s > kClampSpan;
+}
+
+// c rounded toward zero to a multiple of ulp(q), 0 <= c <= q (the grid is clamped to 2^-126: a
+// coarser grid keeps every multiple a multiple of ulp(q))
+__device__ __forceinline__ float round_to_ulp_of(float c, float q) {
+  const int e = __float_as_int(q) & 0x7f800000;
+  const float ulp = __int_as_float(e >= (24 << 23) ? e - (23 << 23) : 0x00800000);
+  return truncf(__fdiv_rn(c, ulp)) * ulp;  // exact: ulp is a power of two
+}
+
+// Tile centre of the centred form.  Row block [a, b], column block [p, q] of the
+// sorted sample (a <= b <= p <= q).  The centre c makes EVERY staged value fl(x_j - c) and every
+// row value fl(x_i - c) exact, so the only per-value roundings left are the dithered ones of
+// fl((x_i - c) s_i) and of the pair arithmetic (an inexact fl(x_j - c) is a fixed shift of a column
+// value shared by all 256 R rows of the tile: systematic on discretised samples):
+//   all values >= 0: c = a, or, if some value exceeds 2a, a rounded toward 0 to a multiple of
+//     ulp(q): every x - c is then a multiple of ulp(x) no larger than x (or Sterbenz-exact);
+//   all values <= 0: the mirror image, c next to q, and the COLUMN block goes to registers
+//     (swap = true) so that |x_i - c| stays within one block;
+//   the tile spans 0: c = 0 (x - 0 is exact), with the block that holds 0 in registers.
+// The row side keeps |x_i - c| <= its block's span (+ ulp(q)), or <= |u| + span when 0 lies between
+// the blocks.  Diagonal tiles (one block) never swap.
+__device__ __forceinline__ float psi_tile_centre(float a, float b, float p, float q, bool diag, bool& swap) {
+  swap = false;
+  if (a >= 0.f) return (q <= 2.f * a) ? a : round_to_ulp_of(a, q);
+  if (q <= 0.f) {
+    swap = !diag;
+    return (a >= 2.f * q) ? q : -round_to_ulp_of(-q, -a);
+  }
+  swap = !diag && b < 0.f && p <= 0.f;
+  return 0.f;
 }
 
 template <int ORDER, bool MASK, bool CENTER = false, bool CLAMP = false>
@@ -195,7 +248,7 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
   for (int k = 0; k < R; ++k) {
     const int64_t i = i0 + k * kPsiThreads + tid;
     const float v = (i < n) ? (LDG ? __ldg(xrows + i) : xrows[i]) : xpad;
-    const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+    const float si = dithered_scale(s, i, n);
     const float vi = CEN ? -__fmul_rn(__fsub_rn(v, cen), si) : v;
     xi[k] = pk2(vi, vi);
     const float p = row_phase(i);
@@ -295,7 +348,7 @@ __device__ __forceinline__ double psi_tile_sum_small(const float* sx, const floa
   const u64 xi = pk2(v, v);
   const float p = row_phase(i);
   const u64 ph = pk2(p, p);
-  const float si = __uint_as_float(__float_as_uint(s) + row_scale_offset(i));
+  const float si = dithered_scale(s, i, n);
   const u64 s2 = pk2(si, si);
   __syncthreads();
   const float4* sx4 = reinterpret_cast<const float4*>(sx + jq);

@@ -18,11 +18,6 @@ from paper_1505_02100_b200 import inputs  # noqa: E402
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 TOL = 1e-5
-# Discretised samples (few distinct differences, e.g. values on a coarse grid or 1e6 + N(0,1)
-# quantised by float32) do not average the per-difference fp32 rounding of u, t and P(t);
-# with the cancellation of these samples (sum|K|/|sum K| ~ 700) the fp32 path is good to
-# ~2e-5 there.  The five BASELINE configurations use TOL.
-TOL_DISCRETE = 5e-5
 
 
 @pytest.fixture(scope="module")
@@ -69,24 +64,48 @@ def test_psi_r_small_sweep(P, oracle_mod, n, r):
         assert rel(got, ref) < TOL, (n, r, g, got, ref)
 
 
-@pytest.mark.parametrize("case", ["mixture", "ties", "offset", "normal_small", "toy"])
+def _grid(n, q, seed):
+    return (np.round(np.random.default_rng(seed).standard_normal(n) / q) * q).astype(np.float32)
+
+
+# Discretised samples (few distinct differences, so the fp32 rounding of each
+# repeated difference must not be systematic): values on coarse grids, integers, 1e6 + N(0,1)
+# quantised by float32 (0.0625 steps), 3e4 + N(0,1) (2^-9 steps), heavy ties
+ADVERSARIAL = {
+    "mixture": lambda: inputs.mixture(20000, 3),
+    "ties": lambda: inputs.ties(12000, 4),
+    "ties20": lambda: inputs.ties(20000, 7, levels=20),
+    "ties60": lambda: inputs.ties(30000, 11, levels=60),
+    "integers": lambda: np.round(inputs.normal(20000, 12, sd=5)).astype(np.float32),
+    "offset": lambda: inputs.offset(12000, 5),
+    "offset3e4": lambda: inputs.offset(20000, 8, base=3.0e4),
+    "grid001": lambda: _grid(20000, 0.001, 31),
+    "grid0001": lambda: _grid(20000, 0.0001, 31),
+    "normal_small": lambda: inputs.normal(2, 6),
+    "toy": lambda: inputs.TOY.astype(np.float32),
+}
+
+
+@pytest.mark.parametrize("case", list(ADVERSARIAL))
 def test_plugin_h_adversarial(P, oracle_mod, case):
-    if case == "mixture":
-        x = inputs.mixture(20000, 3)
-    elif case == "ties":
-        x = inputs.ties(12000, 4)
-    elif case == "offset":
-        x = inputs.offset(12000, 5)
-    elif case == "normal_small":
-        x = inputs.normal(2, 6)
-    else:
-        x = inputs.TOY.astype(np.float32)
+    x = ADVERSARIAL[case]()
     o = oracle_mod.plugin(x)
     r = P.plugin_h_sync(torch.from_numpy(x).cuda())
     assert r["status"] == 0
-    tol = TOL_DISCRETE if case in ("ties", "offset") else TOL
     for key in ("psi6_z", "psi4_z", "h", "g1", "g2", "sigma"):
-        assert rel(r[key], o[key]) < tol, (case, key, r[key], o[key], rel(r[key], o[key]))
+        assert rel(r[key], o[key]) < TOL, (case, key, r[key], o[key], rel(r[key], o[key]))
+
+
+@pytest.mark.parametrize("g", [1.0, 0.5, 2.0 ** -3, 0.999999])
+@pytest.mark.parametrize("r", [4, 6, 8])
+def test_psi_r_power_of_two_scale(P, oracle_mod, g, r):
+    # s = 1/g a power of two: the per-row scale dither s + k ulp(s) must stay symmetric where
+    # s - |k| ulp(s) falls into the binade below (psi_tile.cuh dithered_scale); an oversmoothing
+    # g makes the sum cancel strongly, so a one-sided dilation would show
+    x = inputs.normal(5000, 5040)
+    got = P.psi_r(torch.from_numpy(x).cuda(), g, r).item()
+    ref = oracle_mod.psi(oracle_mod.widen(x), g, r)
+    assert rel(got, ref) < TOL, (g, r, got, ref)
 
 
 def test_two_point_closed_form(P):

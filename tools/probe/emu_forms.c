@@ -1,0 +1,180 @@
+// Dev probe (not product, not oracle): CPU emulation of whole psi-pass evaluation schemes (every
+// fp32 rounding as the GPU does it; exp2 exact on the rounded argument, so the MUFU.EX2 table
+// bias, handled by the per-row phase, is not modelled).  Prints the relative error of each
+// scheme's weighted pair sum against the same sum in fp64 with exact 1/g.
+//   build: gcc -O2 -fopenmp -ffp-contract=off -o /tmp/emuf tools/probe/emu_forms.c -lm
+//   usage: emuf <f32 sorted file> <n> <g> <r> <T> <cmode> <K> <form> [rowstride]
+// cmode: 0 centre = the tile's first row (round-1 kernel), 5 exact-staging centre with the
+//        register/staged roles swapped on negative tiles
+// K:     0 round-1 scale dither (k_i in [-7, 7]); > 0 antithetic k in [-K, K], k_(2m+1) = -k_(2m);
+//        -1 no dither
+// form:  0 t-form (round 1: u, t = u u, a = t c + p, P(t), acc)
+//        1 a-form (v = u sqrt(log2 e / 2), a = p - v v, Q(a) monic with per-row coefficients)
+//        2 a-form with the row offset's low part folded in (a = fma(-v, v, p) - 2 v X_lo)
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static unsigned int row_hash(int64_t i) { return (unsigned int)i * 2654435769u; }
+static float row_phase(int64_t i) { return -1.0f - (float)(row_hash(i) >> 8) * (1.0f / 16777216.0f); }
+static int row_scale_offset(int64_t i) {
+  unsigned int h = ((unsigned int)i * 0x85EBCA6Bu) ^ 0x9E3779B9u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  return (int)(((h >> 16) * 15u) >> 16) - 7;
+}
+static int anti_offset(int64_t i, int K) {
+  unsigned int h = ((unsigned int)(i >> 1) * 0x85EBCA6Bu) ^ 0x9E3779B9u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 13;
+  int k = (int)(h % (unsigned)(2 * K + 1)) - K;
+  return (i & 1) ? -k : k;
+}
+static float u2f(unsigned int u) { float f; memcpy(&f, &u, 4); return f; }
+static unsigned int f2u(float f) { unsigned int u; memcpy(&u, &f, 4); return u; }
+
+static double poly(int r, double t) {
+  if (r == 6) return ((t - 15) * t + 45) * t - 15;
+  if (r == 4) return (t - 6) * t + 3;
+  if (r == 8) return (((t - 28) * t + 210) * t - 420) * t + 105;
+  return 1.0;
+}
+static float polyf(int r, float t) {
+  if (r == 6) return fmaf(fmaf(t - 15.f, t, 45.f), t, -15.f);
+  if (r == 4) return fmaf(t - 6.f, t, 3.f);
+  if (r == 8) return fmaf(fmaf(fmaf(t - 28.f, t, 210.f), t, -420.f), t, 105.f);
+  return 1.f;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 9) return 1;
+  FILE* f = fopen(argv[1], "rb");
+  int64_t n = atoll(argv[2]);
+  double g = atof(argv[3]);
+  int r = atoi(argv[4]);
+  int T = atoi(argv[5]);
+  int cmode = atoi(argv[6]);
+  int K = atoi(argv[7]);
+  int form = atoi(argv[8]);
+  int stride = argc > 9 ? atoi(argv[9]) : 1;
+  float* x = malloc(n * 4);
+  if (fread(x, 4, n, f) != (size_t)n) return 2;
+  fclose(f);
+  const double LOG2E_2 = 0.72134752044448170368;  // log2(e)/2
+  const double GAM = sqrt(LOG2E_2);                // v = u * GAM, v^2 = u^2 log2(e)/2
+  const double LAM = 1.0 / LOG2E_2;                // t = LAM * (p - a)
+  const float c2f = -0.72134752f;
+  const float sf = (float)(1.0 / g);
+  const float sgf = (float)(GAM / g);
+  int64_t nb = (n + T - 1) / T;
+  double tot_ref = 0.0, tot = 0.0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : tot_ref, tot)
+  for (int64_t bi = 0; bi < nb; ++bi) {
+    for (int64_t bj = bi; bj < nb; ++bj) {
+      const int64_t i0 = bi * T, j0 = bj * T;
+      const double w = (bi == bj) ? 1.0 : 2.0;
+      const int64_t il = (i0 + T < n ? i0 + T : n) - 1;
+      const int64_t jl = (j0 + T < n ? j0 + T : n) - 1;
+      float cen = x[i0];
+      int64_t ri0 = i0, rj0 = j0;
+      if (cmode == 5) {
+        const float a = x[i0], b = x[il], pp = x[j0], q = x[jl];
+        if (a >= 0.f) {
+          const float uq = nextafterf(q, INFINITY) - q;
+          cen = truncf(a / uq) * uq;
+        } else if (q <= 0.f) {
+          const float ua = nextafterf(-a, INFINITY) + a;
+          cen = truncf(q / ua) * ua;
+          ri0 = j0; rj0 = i0;
+        } else {
+          cen = 0.f;
+          if (!(b >= 0.f) && pp <= 0.f) { ri0 = j0; rj0 = i0; }
+        }
+      }
+      const int64_t iend = ri0 + T < n ? ri0 + T : n;
+      const int64_t jend = rj0 + T < n ? rj0 + T : n;
+      double tref = 0.0, tgpu = 0.0;
+      for (int64_t i = ri0; i < iend; ++i) {
+        if (stride > 1 && (i % stride) != 0) continue;
+        int k = 0;
+        if (K == 0) k = row_scale_offset(i);
+        else if (K > 0) k = anti_offset(i, K);
+        const float p = row_phase(i);
+        const double comp = exp2(-(double)p);
+        double rref = 0.0, rgpu = 0.0;
+        for (int64_t j = rj0; j < jend; ++j) {
+          double ud = ((double)x[j] - (double)x[i]) / g, td = ud * ud;
+          rref += poly(r, td) * exp(-0.5 * td);
+        }
+        const float xi_c = x[i] - cen;
+        float acc0 = 0.f, acc1 = 0.f;
+        if (form == 0) {
+          const float ulps = u2f((f2u(sf) & 0x7f800000u) - (23u << 23));
+          const float si = fmaf((float)k, ulps, sf);  // s + k ulp(s), exact and symmetric in k
+          const float Xi = -(xi_c * si);
+          for (int64_t j = rj0; j < jend; ++j) {
+            const float xj_c = x[j] - cen;
+            const float u = fmaf(xj_c, si, Xi);
+            const float t = u * u;
+            const float a = fmaf(t, c2f, p);
+            const float e = (float)exp2((double)a);
+            const float P = polyf(r, t);
+            float* ac = ((j - rj0) & 1) ? &acc1 : &acc0;
+            *ac = fmaf(P, e, *ac);
+            if (((j - rj0) & 63) == 63 || j == jend - 1) {
+              rgpu += (double)(acc0 + acc1) * comp;
+              acc0 = acc1 = 0.f;
+            }
+          }
+        } else {
+          const float si = u2f(f2u(sgf) + k);
+          const float Xi = -(xi_c * si);
+          const float Xlo = fmaf(-xi_c, si, -Xi);  // exact: -xi_c si = Xi + Xlo
+          const double pd = p;
+          // monic Q(a) = z^3 + A z^2 + B z + C (r = 6) | z^2 + A z + B (r = 4), z = a - p;
+          // P_r(t) = (-LAM)^(r/2) Q(a)
+          double c[4] = {0, 0, 0, 0};
+          double fac;
+          if (r == 6) {
+            const double A = 15 / LAM, B = 45 / (LAM * LAM), C = 15 / (LAM * LAM * LAM);
+            c[0] = A - 3 * pd;
+            c[1] = 3 * pd * pd - 2 * A * pd + B;
+            c[2] = -pd * pd * pd + A * pd * pd - B * pd + C;
+            fac = -LAM * LAM * LAM;
+          } else {
+            const double A = 6 / LAM, B = 3 / (LAM * LAM);
+            c[0] = A - 2 * pd;
+            c[1] = pd * pd - A * pd + B;
+            fac = LAM * LAM;
+          }
+          const float c0 = (float)c[0], c1 = (float)c[1], c2c = (float)c[2];
+          for (int64_t j = rj0; j < jend; ++j) {
+            const float xj_c = x[j] - cen;
+            const float v = fmaf(xj_c, si, Xi);
+            float a = fmaf(-v, v, p);
+            if (form == 2) a = fmaf(-2.f * Xlo, v, a);
+            const float e = (float)exp2((double)a);
+            float Q;
+            if (r == 6) Q = fmaf(fmaf(a + c0, a, c1), a, c2c);
+            else Q = fmaf(a + c0, a, c1);
+            float* ac = ((j - rj0) & 1) ? &acc1 : &acc0;
+            *ac = fmaf(Q, e, *ac);
+            if (((j - rj0) & 63) == 63 || j == jend - 1) {
+              rgpu += (double)(acc0 + acc1) * comp * fac;
+              acc0 = acc1 = 0.f;
+            }
+          }
+        }
+        tref += rref;
+        tgpu += rgpu;
+      }
+      tot_ref += w * tref;
+      tot += w * tgpu;
+    }
+  }
+  printf("%.17g %.17g %.6e\n", tot_ref, tot, tot / tot_ref - 1.0);
+  return 0;
+}
