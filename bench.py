@@ -638,10 +638,50 @@ def run_batch(a):
     return 0
 
 
+def launch_plan(gpus: int, env: dict, device_count: int) -> tuple[str, str]:
+    """How the repo arm runs N GPUs: ("run", "") when the process is already one of N ranks
+    (or N = 1 without a launcher), ("reexec", "") when N > 1 was asked without torchrun (re-run
+    under torch.distributed.run, one rank per GPU), ("error", why) when the request cannot be
+    honoured -- never one rank labelled N."""
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            return "error", f"--gpus {gpus} but WORLD_SIZE={ws}"
+        return "run", ""
+    if gpus <= 1:
+        return "run", ""
+    if device_count < gpus:
+        return "error", f"--gpus {gpus} needs {gpus} visible CUDA devices, found {device_count}"
+    return "reexec", ""
+
+
+def _reexec_under_torchrun(gpus: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     a = _args()
     if a.impl == "reference":
         return run_reference(a)
+    if a.workload != "plugin" or a.skip_underflow:
+        if a.gpus != 1 or int(os.environ.get("WORLD_SIZE", "1")) != 1:
+            print(f"bench.py: the {a.workload}{' --skip-underflow' if a.skip_underflow else ''} workload runs on "
+                  "one GPU only (--gpus 1)", file=sys.stderr)
+            return 2
+    else:
+        import torch
+        plan, why = launch_plan(a.gpus, dict(os.environ), torch.cuda.device_count())
+        if plan == "error":
+            print(f"bench.py: {why}", file=sys.stderr)
+            return 2
+        if plan == "reexec":
+            return _reexec_under_torchrun(a.gpus)
     if a.workload == "kde":
         return run_kde(a)
     if a.workload in ("q32", "dpi"):

@@ -269,14 +269,16 @@ int64_t oracle_q32_exp(int64_t x) {
 
 /* Q4-Q5: the pair term of Steps IV/VI in Q32.32, K^(r)(u)/phi(0) with u = |d| * rg:
  * t = u^2; 0 if t > 42 (e^{-t/2} = 0 below -21); else P_r(t) * e^{-t/2} with the printed
- * polynomials evaluated by Horner in Q32.32. */
-static int64_t q32_term_c(const int64_t* c, int64_t d, int64_t rg, int r) {
+ * polynomials evaluated by Horner in Q32.32.  a = |d| is the exact
+ * magnitude of the difference of two Q32.32 values (a uint64: no overflow for any pair). */
+static int64_t q32_term_c(const int64_t* c, uint64_t a, int64_t rg, int r) {
   const int64_t one = 4294967296LL;
-  const int64_t a = d < 0 ? -d : d;
-  const int64_t u = oracle_q32_mul(a, rg);
-  /* u > 7 implies t = floor(u^2) > 42, so the term is 0 (reading Q4); testing u first keeps
+  /* u > 7 implies t = floor(u^2) > 42, so the term is 0 (reading Q4).  The test is made on the
+   * exact 128-bit product, before u is narrowed to int64 (|d| rg can exceed 2^95), and keeps
    * floor(u*u / 2^32) inside int64 (it wraps for u >= 46341) */
-  if (u > 7 * one) return 0;
+  const unsigned __int128 ue = ((unsigned __int128)a * (unsigned __int128)(uint64_t)rg) >> 32;
+  if (ue > (unsigned __int128)(7 * one)) return 0;
+  const int64_t u = (int64_t)ue;
   const int64_t t = oracle_q32_mul(u, u);
   if (t > 42 * one) return 0;
   const int64_t e = q32_exp_c(c, -(t >> 1));
@@ -286,10 +288,15 @@ static int64_t q32_term_c(const int64_t* c, int64_t d, int64_t rg, int r) {
   return oracle_q32_mul(P, e);
 }
 
+/* |x - y| of two int64 without overflow */
+static uint64_t q32_absdiff(int64_t x, int64_t y) {
+  return x >= y ? (uint64_t)x - (uint64_t)y : (uint64_t)y - (uint64_t)x;
+}
+
 int64_t oracle_q32_term(int64_t d, int64_t rg, int r) {
   int64_t c[10];
   q32_taylor(c);
-  return q32_term_c(c, d, rg, r);
+  return q32_term_c(c, q32_absdiff(d, 0), rg, r);
 }
 
 /* The halved sum of Eq. 6/7 in Q32.32: out = sum_{i<j} term(z_i - z_j) as an exact int128
@@ -308,7 +315,7 @@ void oracle_q32_psi_sum(const int64_t* zq, int64_t n, int64_t rg, int r, int nth
 #endif
   for (int64_t i = 0; i < n; ++i) {
     i128 acc = 0;
-    for (int64_t j = i + 1; j < n; ++j) acc += q32_term_c(c, zq[i] - zq[j], rg, r);
+    for (int64_t j = i + 1; j < n; ++j) acc += q32_term_c(c, q32_absdiff(zq[i], zq[j]), rg, r);
     row[i] = acc;
   }
   for (int64_t i = 0; i < n; ++i) total += row[i];

@@ -2,6 +2,7 @@
 // fixed-point accumulator, launch declarations).  Product code: nothing here is
 // shared with oracle/.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -74,6 +75,31 @@ struct Layout {
 Layout layout(int64_t n);
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- per-device, set-once host caches (launch geometry, function attributes) --------
+// Keyed by the CURRENT device: occupancy, SM counts and cudaFuncSetAttribute are per device, so
+// a process that calls the library on several GPUs gets each device's own values.  f(dev) must
+// return a value >= 0 and must be idempotent (two threads may both compute it the first time).
+constexpr int kMaxDevices = 64;
+struct DevCache {
+  std::atomic<int> v[kMaxDevices];  // value + 1; 0 = not yet computed (static storage: zeroed)
+};
+template <class F>
+inline int dev_cached(DevCache& c, F f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return f(dev < 0 ? 0 : dev);
+  int v = c.v[dev].load(std::memory_order_acquire);
+  if (v == 0) {
+    v = f(dev) + 1;
+    c.v[dev].store(v, std::memory_order_release);
+  }
+  return v - 1;
+}
+inline int device_sms(int dev) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 1;
+}
 
 // ---- launchers (each returns cudaGetLastError()) ----------------------------------
 cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials, plugin_result* out,

@@ -247,15 +247,13 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
 cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int skip, plugin_result* out,
                          cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  static int max_grid = -1;
-  if (max_grid < 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static DevCache grid_cache;
+  const int max_grid = dev_cached(grid_cache, [](int dev) {
+    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_batch_kernel, kPsiThreads,
                                                   sizeof(float) * 2 * kBlockSortN);
-    max_grid = sms * (occ > 0 ? occ : 1);
-  }
+    return device_sms(dev) * (occ > 0 ? occ : 1);
+  });
   const int grid = count < max_grid ? count : max_grid;
   plugin_batch_kernel<<<grid, kPsiThreads, sizeof(float) * 2 * kBlockSortN, s>>>(x, offsets, count, skip, out);
   return cudaGetLastError();
@@ -263,23 +261,20 @@ cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int 
 
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {
   if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n) != 0) return cudaErrorNotSupported;
-  static int max_grid = -1;
-  if (max_grid < 0) {
-    int dev = 0, sms = 0, occ = 0, coop = 0;
-    cudaGetDevice(&dev);
+  static DevCache grid_cache, sm_cache;
+  const int max_grid = dev_cached(grid_cache, [](int dev) {
+    int occ = 0, coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<0>, kPsiThreads,
                                                   sizeof(float) * 2 * kBlockSortN);
-    max_grid = coop ? sms * occ : 0;
-    if (max_grid > kFusedMaxGrid) max_grid = kFusedMaxGrid;
-  }
+    const int g = coop ? device_sms(dev) * occ : 0;
+    return g > kFusedMaxGrid ? kFusedMaxGrid : g;
+  });
   if (max_grid <= 0) return cudaErrorNotSupported;
   const int64_t T = kPsiSmallT, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
   int nsx = (int)(nb * T > kBlockSortN ? nb * T : kBlockSortN);  // cta_sort2048 writes 2048 positions
   // one CTA per SM at most: every CTA sorts its own copy of X, so more CTAs than SMs add no speed
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = dev_cached(sm_cache, device_sms);
   int grid = (int)(tiles < max_grid ? tiles : max_grid);
   if (grid > sms) grid = sms;
   size_t smem = sizeof(float) * ((size_t)nsx + kBlockSortN);  // sample + sort scratch

@@ -181,14 +181,12 @@ template <int R, int ORDER>
 static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, const double* g_dev,
                             const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tb, int64_t te, cudaStream_t s,
                             PsiFin fin) {
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static DevCache cap_cache;
+  const int grid_cap = dev_cached(cap_cache, [](int dev) {
+    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_kernel<R, ORDER>, kPsiThreads, 0);
-    grid_cap = sms * (occ > 0 ? occ : 1);
-  }
+    return device_sms(dev) * (occ > 0 ? occ : 1);
+  });
   int64_t tiles = te - tb;
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;

@@ -56,13 +56,17 @@ __device__ __forceinline__ long long q32_exp(long long x) {
   return sh >= 63 ? 0 : (p >> sh);
 }
 
-// K^(r)(u)/phi(0) in Q32.32 for the pair difference d (Q4-Q5)
+// K^(r)(u)/phi(0) in Q32.32 for the pair zi, zj (Q4-Q5): a = |zi - zj| exactly (uint64, no
+// overflow for any two int64), u = floor(a rg / 2^32) tested against 7 on the exact 128-bit
+// product before it is narrowed (|d| rg can exceed 2^95 for arbitrary psi_r_q32 inputs)
 template <int ORDER>
-__device__ __forceinline__ long long q32_term(long long d, long long rg) {
+__device__ __forceinline__ long long q32_term(long long zi, long long zj, long long rg) {
   const long long one = 4294967296LL;
-  const long long a = d < 0 ? -d : d;
-  const long long u = q32_mul(a, rg);
-  if (u > 7 * one) return 0;  // then t > 42 too; and u*u would leave int64 for u >= 46341
+  const unsigned long long a = zi >= zj ? (unsigned long long)zi - (unsigned long long)zj
+                                        : (unsigned long long)zj - (unsigned long long)zi;
+  const unsigned __int128 ue = ((unsigned __int128)a * (unsigned __int128)(unsigned long long)rg) >> 32;
+  if (ue > (unsigned __int128)(7 * one)) return 0;  // then t > 42 too; and u*u would leave int64 for u >= 46341
+  const long long u = (long long)ue;
   const long long t = q32_mul(u, u);
   if (t > 42 * one) return 0;  // e^{-t/2} below the e^-21 clamp
   const long long e = q32_exp(-(t >> 1));
@@ -117,7 +121,7 @@ psi_q32_kernel(const long long* __restrict__ zq, int64_t n, long long rg_host, c
       const int64_t i = i0 + k * kPsiThreads + tid;
       if (i >= n) continue;
       long long acc = 0;
-      for (int j = 0; j < jcount; ++j) acc += q32_term<ORDER>(zi[k] - sz[j], rg);
+      for (int j = 0; j < jcount; ++j) acc += q32_term<ORDER>(zi[k], sz[j], rg);
       tsum += acc;
     }
     // weight: off-diagonal tiles count (i, j) and (j, i)
@@ -190,14 +194,12 @@ __global__ void q32_encode_kernel(const float* __restrict__ xs, int64_t n, const
 cudaError_t launch_psi_q32(const long long* zq, int64_t n, long long rg_host, const long long* rg_dev,
                            const int32_t* status_dev, int r, Ctrl* ctrl, int slot, long long* out, int what,
                            plugin_result* res, long long* rg_next, cudaStream_t s) {
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static DevCache cap_cache;
+  const int grid_cap = dev_cached(cap_cache, [](int dev) {
+    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_q32_kernel<6>, kPsiThreads, 0);
-    grid_cap = sms * (occ > 0 ? occ : 1);
-  }
+    return device_sms(dev) * (occ > 0 ? occ : 1);
+  });
   const int64_t nb = (n + kQ32T - 1) / kQ32T, tiles = nb * (nb + 1) / 2;
   const int grid = (int)(tiles < grid_cap ? (tiles < 1 ? 1 : tiles) : grid_cap);
   if (r == 6) psi_q32_kernel<6><<<grid, kPsiThreads, 0, s>>>(zq, n, rg_host, rg_dev, status_dev, ctrl, slot);

@@ -277,14 +277,14 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
     const int nblocks = (int)((n + kBlockSortN - 1) / kBlockSortN);
     sort_block_kernel<<<nblocks, 256, 0, s>>>(x, n, tmp, xs);
     if (nblocks > 1) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(sort_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(unsigned int) * kBlockSortMax));
-        attr = true;
-      }
-      const int64_t want = (n + 255) / 256;
-      sort_merge_kernel<<<(unsigned)(want < 148 ? want : 148), 256, sizeof(unsigned int) * (size_t)n, s>>>(
+      static DevCache attr_cache;  // the opt-in is a per-device function attribute
+      dev_cached(attr_cache, [](int) {
+        return (int)cudaFuncSetAttribute(sort_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(unsigned int) * kBlockSortMax));
+      });
+      static DevCache sm_cache;
+      const int64_t want = (n + 255) / 256, sms = dev_cached(sm_cache, device_sms);
+      sort_merge_kernel<<<(unsigned)(want < sms ? want : sms), 256, sizeof(unsigned int) * (size_t)n, s>>>(
           tmp, n, nblocks, xs);
     }
     return cudaGetLastError();

@@ -47,18 +47,23 @@ def plugin_h_distributed(x: torch.Tensor, group=None, out: torch.Tensor | None =
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     n = x.numel()
-    ws = P.workspace(n, x.device) if ws is None else ws
-    out = P.new_result(x.device) if out is None else out
-    P.plugin_step1(x, out, ws, stream)
-    for r, after in ((6, P.plugin_after_psi6), (4, P.plugin_after_psi4)):
-        part = P.new_partial(x.device)
-        ev = events.get(f"psi{r}") if events else None
-        if ev:
-            ev[0].record()
-        P.psi_r_shard(n, r, rank, world, out, part, ws, stream)
-        if ev:
-            ev[1].record()
-        if world > 1:
-            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
-        after(part, out, stream)
+    # everything (the library calls, the NCCL allreduce, the events, the temporaries) on ONE
+    # stream, made current: the collective then reads each partial after its shard wrote it,
+    # and the finalize reads the reduced total after the collective
+    with P._On(x.device, stream) as on:
+        s = on.stream
+        ws = P.workspace(n, x.device) if ws is None else ws
+        out = P.new_result(x.device) if out is None else out
+        P.plugin_step1(x, out, ws, s)
+        for r, after in ((6, P.plugin_after_psi6), (4, P.plugin_after_psi4)):
+            part = P.new_partial(x.device)
+            ev = events.get(f"psi{r}") if events else None
+            if ev:
+                ev[0].record(s)
+            P.psi_r_shard(n, r, rank, world, out, part, ws, s)
+            if ev:
+                ev[1].record(s)
+            if world > 1:
+                dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+            after(part, out, s)
     return out

@@ -124,12 +124,52 @@ def _check(st: int):
     return st
 
 
-def _stream(stream):
-    if stream is None:
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    if isinstance(stream, torch.cuda.Stream):
-        return ctypes.c_void_p(stream.cuda_stream)
-    return ctypes.c_void_p(int(stream))
+def _dev(t: torch.Tensor) -> torch.device:
+    """The device of a tensor argument (checked like _x, without copying)."""
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError("expected a CUDA tensor")
+    return t.device
+
+
+class _On:
+    """Run a library call on the device of its input and on `stream` (None: that device's
+    current stream; a torch.cuda.Stream; or a raw cudaStream_t handle).  Inside the block the
+    device and the stream are current, so temporaries (workspace, contiguous copies, outputs)
+    are allocated for that stream and the caching allocator cannot hand them out again while
+    the library's kernels on it still use them."""
+
+    def __init__(self, device, stream=None):
+        self.device = torch.device(device)
+        if stream is None:
+            self.stream = torch.cuda.current_stream(self.device)
+        elif isinstance(stream, torch.cuda.Stream):
+            self.stream = stream
+        else:
+            self.stream = torch.cuda.ExternalStream(int(stream), device=self.device)
+
+    def __enter__(self):
+        self._dev = torch.cuda.device(self.device)
+        self._dev.__enter__()
+        self._st = torch.cuda.stream(self.stream)
+        self._st.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        self._st.__exit__(*exc)
+        self._dev.__exit__(*exc)
+        return False
+
+    @property
+    def handle(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def uses(self, *tensors):
+        """Mark caller-owned inputs as used on this stream (Tensor.record_stream): the caching
+        allocator then keeps their memory until the library's kernels on it have run, even if
+        the caller drops its last reference right after the (asynchronous) call."""
+        for t in tensors:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(self.stream)
 
 
 def _x(x: torch.Tensor) -> torch.Tensor:
@@ -168,12 +208,13 @@ def plugin_h(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor 
              flags: int = 0):
     """Alg. 1 on the device (asynchronous).  Returns the device result buffer.
     ``flags``: PLUGIN_SKIP_UNDERFLOW (bit-identical result, less work; plugin_h_ex)."""
-    x = _x(x)
-    n = x.numel()
-    ws = workspace(n, x.device) if ws is None else ws
-    out = new_result(x.device) if out is None else out
-    _check(lib().plugin_h_ex(x.data_ptr(), n, out.data_ptr(), int(flags), ws.data_ptr(), ws.numel(),
-                             _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        ws = workspace(n, x.device) if ws is None else ws
+        out = new_result(x.device) if out is None else out
+        _check(lib().plugin_h_ex(x.data_ptr(), n, out.data_ptr(), int(flags), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 
@@ -182,14 +223,15 @@ def plugin_h_batch(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | N
     """Alg. 1 for every sample x[offsets[b]:offsets[b+1]] (2 <= n_b <= 2048), one CTA each
     (T = 256 tiles: agrees with plugin_h to fp32 rounding); returns the device buffer of count
     plugin_result records (read_results decodes it)."""
-    x = _x(x)
     if not (isinstance(offsets, torch.Tensor) and offsets.is_cuda and offsets.dtype == torch.int64):
         raise TypeError("offsets must be a CUDA int64 tensor of count + 1 entries")
-    offsets = offsets.contiguous()
-    count = offsets.numel() - 1
-    out = torch.empty(max(count, 1) * RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
-    _check(lib().plugin_h_batch(x.data_ptr(), offsets.data_ptr(), count, out.data_ptr(), int(flags),
-                                _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        offsets = offsets.contiguous()
+        count = offsets.numel() - 1
+        out = torch.empty(max(count, 1) * RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
+        _check(lib().plugin_h_batch(x.data_ptr(), offsets.data_ptr(), count, out.data_ptr(), int(flags), on.handle))
     return out
 
 
@@ -199,17 +241,24 @@ class PluginGraph:
 
     def __init__(self, x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
                  flags: int = 0):
+        self.handle = None
         self.x = _x(x)
-        n = self.x.numel()
-        self.ws = workspace(n, self.x.device) if ws is None else ws
-        self.out = new_result(self.x.device) if out is None else out
-        h = ctypes.c_void_p()
-        _check(lib().plugin_graph_create(self.x.data_ptr(), n, self.out.data_ptr(), self.ws.data_ptr(),
-                                         self.ws.numel(), int(flags), ctypes.byref(h)))
+        self.device = self.x.device
+        with torch.cuda.device(self.device):
+            n = self.x.numel()
+            self.ws = workspace(n, self.device) if ws is None else ws
+            self.out = new_result(self.device) if out is None else out
+            h = ctypes.c_void_p()
+            _check(lib().plugin_graph_create(self.x.data_ptr(), n, self.out.data_ptr(), self.ws.data_ptr(),
+                                             self.ws.numel(), int(flags), ctypes.byref(h)))
         self.handle = h
 
     def launch(self, stream=None) -> torch.Tensor:
-        _check(lib().plugin_graph_launch(self.handle, _stream(stream)))
+        # no temporaries here: only the stream needs resolving (kept light: latency path)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        h = stream.cuda_stream if isinstance(stream, torch.cuda.Stream) else int(stream)
+        _check(lib().plugin_graph_launch(self.handle, ctypes.c_void_p(h)))
         return self.out
 
     def close(self):
@@ -230,11 +279,13 @@ def read_results(buf: torch.Tensor, count: int) -> list[dict]:
 
 
 def plugin_h_sync(x: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> dict:
-    x = _x(x)
-    n = x.numel()
-    ws = workspace(n, x.device) if ws is None else ws
-    res = plugin_result()
-    _check(lib().plugin_h_sync(x.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        ws = workspace(n, x.device) if ws is None else ws
+        res = plugin_result()
+        _check(lib().plugin_h_sync(x.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(), on.handle))
     return res.to_dict()
 
 
@@ -244,27 +295,32 @@ def plugin_h_host(x_host: torch.Tensor, ws: torch.Tensor | None = None, stream=N
         raise TypeError("x_host must be a CPU float32 tensor (pinned for best speed)")
     x_host = x_host.contiguous()
     n = x_host.numel()
-    ws = workspace(n, "cuda", host=True) if ws is None else ws
-    res = plugin_result()
-    _check(lib().plugin_h_host(x_host.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(),
-                               _stream(stream)))
+    dev = ws.device if ws is not None else torch.device("cuda", torch.cuda.current_device())
+    with _On(dev, stream) as on:
+        ws = workspace(n, dev, host=True) if ws is None else ws
+        res = plugin_result()
+        _check(lib().plugin_h_host(x_host.data_ptr(), n, ctypes.addressof(res), ws.data_ptr(), ws.numel(), on.handle))
     return res.to_dict()
 
 
 def psi_r(x: torch.Tensor, g: float, r: int, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
           stream=None) -> torch.Tensor:
     """Psi_r(g) (Steps IV/VI) as a device float64[1] tensor (asynchronous)."""
-    x = _x(x)
-    n = x.numel()
-    ws = workspace(n, x.device) if ws is None else ws
-    out = torch.empty(1, dtype=torch.float64, device=x.device) if out is None else out
-    _check(lib().psi_r(x.data_ptr(), n, float(g), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        ws = workspace(n, x.device) if ws is None else ws
+        out = torch.empty(1, dtype=torch.float64, device=x.device) if out is None else out
+        _check(lib().psi_r(x.data_ptr(), n, float(g), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 
 def plugin_step1(x: torch.Tensor, out: torch.Tensor, ws: torch.Tensor, stream=None):
-    x = _x(x)
-    _check(lib().plugin_step1(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        _check(lib().plugin_step1(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 
@@ -274,18 +330,21 @@ def new_partial(device=None) -> torch.Tensor:
 
 def psi_r_shard(n: int, r: int, rank: int, world: int, out: torch.Tensor, partial: torch.Tensor, ws: torch.Tensor,
                 stream=None):
-    _check(lib().psi_r_shard(n, r, rank, world, out.data_ptr(), partial.data_ptr(), ws.data_ptr(), ws.numel(),
-                             _stream(stream)))
+    with _On(ws.device, stream) as on:
+        _check(lib().psi_r_shard(n, r, rank, world, out.data_ptr(), partial.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 on.handle))
     return partial
 
 
 def plugin_after_psi6(total: torch.Tensor, out: torch.Tensor, stream=None):
-    _check(lib().plugin_after_psi6(total.data_ptr(), out.data_ptr(), _stream(stream)))
+    with _On(out.device, stream) as on:
+        _check(lib().plugin_after_psi6(total.data_ptr(), out.data_ptr(), on.handle))
     return out
 
 
 def plugin_after_psi4(total: torch.Tensor, out: torch.Tensor, stream=None):
-    _check(lib().plugin_after_psi4(total.data_ptr(), out.data_ptr(), _stream(stream)))
+    with _On(out.device, stream) as on:
+        _check(lib().plugin_after_psi4(total.data_ptr(), out.data_ptr(), on.handle))
     return out
 
 
@@ -305,12 +364,13 @@ DPI_RESULT_BYTES = ctypes.sizeof(plugin_dpi_result)
 def plugin_dpi(x: torch.Tensor, stages: int, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
                stream=None) -> torch.Tensor:
     """l-stage direct plug-in (Alg. 1 is stages = 2) on the device; returns the result buffer."""
-    x = _x(x)
-    n = x.numel()
-    ws = workspace(n, x.device) if ws is None else ws
-    out = torch.empty(DPI_RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
-    _check(lib().plugin_dpi(x.data_ptr(), n, int(stages), out.data_ptr(), ws.data_ptr(), ws.numel(),
-                            _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        ws = workspace(n, x.device) if ws is None else ws
+        out = torch.empty(DPI_RESULT_BYTES, dtype=torch.uint8, device=x.device) if out is None else out
+        _check(lib().plugin_dpi(x.data_ptr(), n, int(stages), out.data_ptr(), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 
@@ -322,27 +382,31 @@ def psi_r_q32(zq: torch.Tensor, rg_q: int, r: int, ws: torch.Tensor | None = Non
     """sum_i sum_j term(zq_i - zq_j) in Q32.32 (NEXT 2) as an exact Python int (synchronises)."""
     if not (isinstance(zq, torch.Tensor) and zq.is_cuda and zq.dtype == torch.int64 and zq.dim() == 1):
         raise TypeError("zq must be a 1-D CUDA int64 tensor (Q32.32 raw values)")
-    zq = zq.contiguous()
-    n = zq.numel()
-    ws = workspace(n, zq.device) if ws is None else ws
-    out = torch.zeros(2, dtype=torch.int64, device=zq.device)
-    _check(lib().psi_r_q32(zq.data_ptr(), n, int(rg_q), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(),
-                           _stream(stream)))
-    lo, hi = out.cpu().tolist()
+    with _On(zq.device, stream) as on:
+        zq = zq.contiguous()
+        on.uses(zq)
+        n = zq.numel()
+        ws = workspace(n, zq.device) if ws is None else ws
+        out = torch.zeros(2, dtype=torch.int64, device=zq.device)
+        _check(lib().psi_r_q32(zq.data_ptr(), n, int(rg_q), int(r), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                               on.handle))
+        lo, hi = out.cpu().tolist()
     return hi * (1 << 64) + (lo & ((1 << 64) - 1))
 
 
 def plugin_h_q32(x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
     """Alg. 1 with the Q32.32 pair passes (asynchronous); returns the device result buffer."""
-    x = _x(x)
-    n = x.numel()
-    if ws is None:
-        nbytes = lib().plugin_q32_workspace_bytes(n)
-        t = torch.empty(nbytes + 256, dtype=torch.uint8, device=x.device)
-        off = (-t.data_ptr()) % 256
-        ws = t[off:off + nbytes]
-    out = new_result(x.device) if out is None else out
-    _check(lib().plugin_h_q32(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        if ws is None:
+            nbytes = lib().plugin_q32_workspace_bytes(n)
+            t = torch.empty(nbytes + 256, dtype=torch.uint8, device=x.device)
+            off = (-t.data_ptr()) % 256
+            ws = t[off:off + nbytes]
+        out = new_result(x.device) if out is None else out
+        _check(lib().plugin_h_q32(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 
@@ -360,40 +424,49 @@ def kde_workspace(n: int, m: int, device=None) -> torch.Tensor:
 def kde_eval(x: torch.Tensor, h: float, points: torch.Tensor, out: torch.Tensor | None = None,
              ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """f(x_k, h) of Eq. 1-2 at every point (device float64[m], asynchronous)."""
-    x = _x(x)
-    points = _x(points)
-    n, m = x.numel(), points.numel()
-    ws = kde_workspace(n, m, x.device) if ws is None else ws
-    out = torch.empty(m, dtype=torch.float64, device=x.device) if out is None else out
-    _check(lib().kde_eval(x.data_ptr(), n, float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(),
-                          ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        points = _x(points)
+        on.uses(points)
+        n, m = x.numel(), points.numel()
+        ws = kde_workspace(n, m, x.device) if ws is None else ws
+        out = torch.empty(m, dtype=torch.float64, device=x.device) if out is None else out
+        _check(lib().kde_eval(x.data_ptr(), n, float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(),
+                              ws.numel(), on.handle))
     return out
 
 
 def kde_prepare(x: torch.Tensor, ws: torch.Tensor, stream=None) -> torch.Tensor:
     """Sort X into the KDE workspace once (then kde_eval_prepared for any points / h)."""
-    x = _x(x)
-    _check(lib().kde_prepare(x.data_ptr(), x.numel(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        _check(lib().kde_prepare(x.data_ptr(), x.numel(), ws.data_ptr(), ws.numel(), on.handle))
     return ws
 
 
 def kde_eval_prepared(n: int, h: float, points: torch.Tensor, ws: torch.Tensor, out: torch.Tensor | None = None,
                       stream=None) -> torch.Tensor:
-    points = _x(points)
-    m = points.numel()
-    out = torch.empty(m, dtype=torch.float64, device=points.device) if out is None else out
-    _check(lib().kde_eval_prepared(int(n), float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                   _stream(stream)))
+    with _On(_dev(points), stream) as on:
+        points = _x(points)
+        on.uses(points, ws)
+        m = points.numel()
+        out = torch.empty(m, dtype=torch.float64, device=points.device) if out is None else out
+        _check(lib().kde_eval_prepared(int(n), float(h), points.data_ptr(), m, out.data_ptr(), ws.data_ptr(),
+                                       ws.numel(), on.handle))
     return out
 
 
 def plugin_sort(x: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """The sorted copy of X the passes read (device float32, asynchronous)."""
-    x = _x(x)
-    n = x.numel()
-    ws = workspace(n, x.device) if ws is None else ws
-    out = torch.empty_like(x)
-    _check(lib().plugin_sort(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        n = x.numel()
+        ws = workspace(n, x.device) if ws is None else ws
+        out = torch.empty_like(x)
+        _check(lib().plugin_sort(x.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), on.handle))
     return out
 
 

@@ -54,3 +54,27 @@ def test_kde_terms_visited_counts_the_window():
         d = np.abs(p[:, None] - xs[None, ~inside])
         assert d.size == 0 or d.min() > cut * (1 - 1e-9)
     assert got == ref
+
+
+def test_launch_plan_never_runs_one_rank_labelled_n():
+    # --gpus N outside torchrun: re-exec with N ranks, or refuse; inside: WORLD_SIZE must match
+    assert bench.launch_plan(1, {}, 0) == ("run", "")
+    assert bench.launch_plan(2, {}, 8)[0] == "reexec"
+    assert bench.launch_plan(8, {}, 8)[0] == "reexec"
+    assert bench.launch_plan(2, {}, 1)[0] == "error"
+    assert bench.launch_plan(4, {"WORLD_SIZE": "4"}, 8) == ("run", "")
+    assert bench.launch_plan(2, {"WORLD_SIZE": "1"}, 8)[0] == "error"
+    assert bench.launch_plan(1, {"WORLD_SIZE": "1"}, 8) == ("run", "")
+
+
+def test_bench_gpus_2_without_gpus_fails_loudly():
+    # on this CPU-only box `bench.py --gpus 2` must exit non-zero with a reason, not measure
+    # one process and label it 2 GPUs
+    import subprocess
+    import sys
+    p = subprocess.run([sys.executable, bench.__file__, "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, env={k: v for k, v in __import__("os").environ.items()
+                                                                         if k not in ("WORLD_SIZE", "RANK")})
+    assert p.returncode != 0
+    assert "needs 2 visible CUDA devices" in p.stderr
+    assert p.stdout.strip() == ""

@@ -65,6 +65,16 @@ class _FakePlugin:
         self.real = real
         self.totals = {}
 
+    class _On:  # the device / stream context of the binding: nothing to switch on CPU
+        def __init__(self, device, stream=None):
+            self.stream = stream
+
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *exc):
+            return False
+
     def workspace(self, n, device=None):
         return torch.zeros(1, dtype=torch.uint8)
 

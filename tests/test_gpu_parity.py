@@ -522,3 +522,36 @@ def test_data_errors_multi_kernel(P, n):
     ok = P.read_result(g.launch())
     assert ok["status"] == 0 and ok["h"] == P.plugin_h_sync(x)["h"]
     g.close()
+
+
+def test_plugin_h_concurrent_streams_distinct_workspaces(P):
+    # the header's promise: calls on different streams with distinct workspaces may run
+    # concurrently.  Two samples (n = 16384: block sort + rank merge with the dynamic-smem
+    # opt-in; n = 40000: radix sort) interleaved on two streams, three rounds, against
+    # sequential runs; temporaries of the binding are allocated on the call's stream
+    xs = [inputs.config_data(2), inputs.mixture(40000, 77)]
+    ref = [P.plugin_h_sync(torch.from_numpy(x).cuda()) for x in xs]
+    streams = (torch.cuda.Stream(), torch.cuda.Stream())
+    bufs = []
+    for _ in range(3):
+        for k, (x, s) in enumerate(zip(xs, streams)):
+            with torch.cuda.stream(s):  # the input is produced on the stream that consumes it
+                xt = torch.from_numpy(x).cuda()
+            st = s if k == 0 else s.cuda_stream  # a torch stream and a raw cudaStream_t handle
+            # the caller drops xt right away: the binding's record_stream keeps its memory alive
+            bufs.append((k, P.plugin_h(xt, stream=st)))
+            del xt
+    torch.cuda.synchronize()
+    for k, b in bufs:
+        got = P.read_result(b)
+        assert _same(got, ref[k]), (k, got["h"], ref[k]["h"])
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_plugin_h_on_a_second_device(P):
+    # per-device launch caches (occupancy, the sort-merge smem opt-in, SM counts): the same
+    # sample on cuda:1 after cuda:0 gives the same bits
+    x = inputs.mixture(20000, 78)
+    a = P.plugin_h_sync(torch.from_numpy(x).to("cuda:0"))
+    b = P.plugin_h_sync(torch.from_numpy(x).to("cuda:1"))
+    assert _same(a, b)

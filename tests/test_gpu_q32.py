@@ -107,3 +107,13 @@ def test_psi_q32_far_pairs_bit_exact(P, oracle_mod):
     rg = ONE
     got = P.psi_r_q32(torch.from_numpy(zq).cuda(), rg, 4)
     assert got == 2 * oracle_mod.q32_psi_sum(zq, rg, 4) + zq.size * oracle_mod.q32_term(0, rg, 4)
+
+
+def test_psi_q32_extreme_values_bit_exact(P, oracle_mod):
+    # Q32.32 values near the int64 limits (|d| rg >= 2^95): their pairs are far (term 0) on
+    # both sides, judged on the exact product (q32.cu q32_term), never on a wrapped one
+    zq = oracle_mod.q32_encode(np.random.default_rng(6).normal(0, 1, 2000))
+    zq = np.concatenate([zq, np.array([(1 << 62), -(1 << 62), (1 << 63) - 1, -(1 << 63)], dtype=np.int64)])
+    for rg in (ONE, (1 << 51) + 12345):
+        got = P.psi_r_q32(torch.from_numpy(zq).cuda(), rg, 6)
+        assert got == 2 * oracle_mod.q32_psi_sum(zq, rg, 6) + zq.size * oracle_mod.q32_term(0, rg, 6)

@@ -80,6 +80,33 @@ def test_term_against_fp64_kernel(oracle_mod, r):
 
 
 @pytest.mark.parametrize("r", [4, 6])
+def test_term_of_far_and_extreme_pairs_is_zero(oracle_mod, r):
+    # reading Q4: the term is 0 once u = |d| rg > 7 (t > 42), judged on the exact product: with
+    # |d| rg >= 2^95 the Q32.32 value of u does not fit int64 and must not wrap into range
+    big = (1 << 63) - 1
+    for d, rg in ((1 << 40, 3 * ONE), (1 << 62, 1 << 51), (big, (1 << 52) - 1), (-big - 1, 1 << 33),
+                  (8 * ONE, ONE), (7 * ONE + 1, ONE)):
+        exact_u = Fraction(abs(d) * rg, ONE * ONE)
+        assert exact_u > 7
+        assert oracle_mod.q32_term(d, rg, r) == 0, (d, rg)
+    # just inside: u = 6.5 gives t = 42.25 > 42 -> 0; u = 6 gives a tiny non-zero term
+    assert oracle_mod.q32_term(6 * ONE, ONE, r) != 0
+
+
+@pytest.mark.parametrize("r", [4, 6])
+def test_halved_sum_of_extreme_values_drops_far_pairs(oracle_mod, r):
+    # values near the int64 limits: every pair with an extreme member is far (term 0), so the
+    # sum equals the sum over the ordinary values alone (no wrapped differences)
+    zq = oracle_mod.q32_encode(inputs.normal(40, 8))
+    ext = np.array([(1 << 62), -(1 << 62), (1 << 63) - 1], dtype=np.int64)
+    rg = ONE
+    both = oracle_mod.q32_psi_sum(np.concatenate([zq, ext]), rg, r)
+    extp = oracle_mod.q32_psi_sum(ext, rg, r)
+    assert both == oracle_mod.q32_psi_sum(zq, rg, r) + extp
+    assert extp == 0
+
+
+@pytest.mark.parametrize("r", [4, 6])
 def test_halved_sum_equals_literal_double_sum_exactly(oracle_mod, r):
     # Eq. 5-7 in integers: sum_i sum_j term = 2 sum_{i<j} term + n term(0), bit for bit
     zq = oracle_mod.q32_encode(inputs.normal(60, 4))

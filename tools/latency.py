@@ -84,6 +84,12 @@ def main():
         pg = P.PluginGraph(x, out=out, ws=ws)
         med, mn = dev_time(lambda: pg.launch(), a.reps)
         row["plugin_graph_us"], row["plugin_graph_min_us"] = med, mn
+        # device time per call with the queue kept full: 50 back-to-back plugin_graph_launch
+        # between two events (the host-side call overhead overlaps the previous run)
+        med, mn = dev_time(lambda: [pg.launch() for _ in range(50)], max(10, a.reps // 10))
+        row["plugin_graph_pipelined_us"], row["plugin_graph_pipelined_min_us"] = med / 50, mn / 50
+        med, mn = dev_time(lambda: [P.plugin_h(x, out=out, ws=ws) for _ in range(50)], max(10, a.reps // 10))
+        row["default_pipelined_us"], row["default_pipelined_min_us"] = med / 50, mn / 50
         pg.close()
         row["h"] = h_default
         row["same_h_all_paths"] = P.read_result(out)["h"] == h_default
