@@ -155,9 +155,12 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
 plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
                            void* d_ws, size_t ws_bytes, void* stream);
 
-/* One rank's share of a psi pass: the tiles [w*rank/world, w*(rank+1)/world) of the
- * pair triangle (w = plugin_num_tiles(n)), at the bandwidth of d_out (g1 for r=6,
- * g2 for r=4), written as an unnormalised fixed-point sum to *d_partial.
+/* One rank's share of a psi pass (Steps IV/VI, Eq. 6/7):
+ * the tiles [w*rank/world, w*(rank+1)/world) of the pair triangle (w = plugin_num_tiles(n)),
+ * at the bandwidth of d_out (g1 for r=6, g2 for r=4), written as an unnormalised fixed-point
+ * sum to *d_partial.  The tiles partition the pairs (sorted sample, upper block triangle,
+ * diagonal tiles as full squares) identically for every world, and sums are exact integers:
+ * any world gives the single-GPU bits.
  * Requires plugin_step1 (and plugin_after_psi6 for r=4) on the same workspace. */
 plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_result* d_out,
                           plugin_fx128* d_partial, void* d_ws, size_t ws_bytes, void* stream);
@@ -167,10 +170,15 @@ plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_re
 plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 
-/* Number of equal-work tiles of the pair triangle for n, and the tile range
- * [begin, end) that `rank` of `world` owns (what psi_r_shard processes). */
+/* Number of equal-work tiles of the pair triangle for n (a function of n only: T x T tiles
+ * of the sorted sample's upper block triangle, T = plugin_tile_edge(n)), and the
+ * tile range [begin, end) that `rank` of `world` owns (what psi_r_shard processes).
+ * Host-only; no CUDA call. */
 int64_t plugin_num_tiles(int64_t n);
 void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
+/* The tile edge T of the pass for n (64 for n <= 2048, else 256 R with R the rows per
+ * thread): the geometry of the tiles above (host-only; for tests and tools). */
+int64_t plugin_tile_edge(int64_t n);
 
 /* ---- the l-stage direct plug-in family ---- */
 

@@ -99,7 +99,9 @@ size_t plugin_host_workspace_bytes(int64_t n) {
   return layout(n).total + align_up(sizeof(float) * (size_t)(n > 0 ? n : 1), 256);
 }
 
-int64_t plugin_num_tiles(int64_t n) { return n > 0 ? psi_tiles(n) : 0; }
+int64_t plugin_num_tiles(int64_t n) { return n > 0 ? psi_work_units(n) : 0; }
+
+int64_t plugin_tile_edge(int64_t n) { return n > 0 ? psi_tile_edge(n) : 0; }
 
 void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end) {
   int64_t w = plugin_num_tiles(n);
@@ -108,7 +110,7 @@ void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t*
     if (end) *end = 0;
     return;
   }
-  // equal-work tiles: contiguous, balanced to within one tile
+  // equal-work items (tiles for n <= 2048, else work units): contiguous, balanced to within one
   if (begin) *begin = (w * rank) / world;
   if (end) *end = (w * (rank + 1)) / world;
 }
@@ -142,7 +144,7 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
     (void)cudaGetLastError();  // not applicable here: take the multi-kernel path
   }
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
-  const int64_t tiles = psi_tiles(n);
+  const int64_t tiles = psi_work_units(n);
   // each pass finalises itself in its last CTA (Steps V / VII; PsiFin)
   PsiFin f6, f4;
   f6.what = 0, f6.out = d_out, f6.r = 6;
@@ -212,7 +214,7 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
   PsiFin fin;  // Psi_r(g) written by the pass's last CTA
   fin.what = 2, fin.g = g, fin.r = r, fin.d_psi = d_psi;
-  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_tiles(n), s, fin)) != cudaSuccess)
+  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_work_units(n), s, fin)) != cudaSuccess)
     return cuda_fail(e, "psi");
   return PLUGIN_OK;
 }
@@ -364,7 +366,7 @@ plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_res
   if ((st = run_step1(d_x, n, s1, w, s)) != PLUGIN_OK) return st;
   cudaError_t e;
   if ((e = launch_dpi_init(s1, stages, d_out, s)) != cudaSuccess) return cuda_fail(e, "dpi init");
-  const int64_t tiles = psi_tiles(n);
+  const int64_t tiles = psi_work_units(n);
   for (int j = stages; j >= 1; --j) {
     const int slot = j & 1;
     if ((e = launch_psi(w.xs, n, 2 * j + 2, 0, 0.0, &d_out->g[j - 1], &d_out->status, w.ctrl, slot, 0, tiles, s)) !=

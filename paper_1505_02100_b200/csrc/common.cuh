@@ -45,6 +45,9 @@ inline int64_t psi_tile_edge(int64_t n) {
 }
 inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
+// the pass's schedulable work items for n samples (a function of n only): its tiles; launch_psi
+// ranges and the multi-GPU shards (plugin_shard_tiles) count these
+int64_t psi_work_units(int64_t n);
 
 // order-preserving float bits <-> uint32 radix key (sort.cu, fused.cu)
 __device__ __forceinline__ unsigned int bits2key(unsigned int b) {

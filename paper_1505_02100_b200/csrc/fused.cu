@@ -217,24 +217,19 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
             ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
           continue;
         const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-        // tile centre and register/staged roles as in psi.cu (psi_tile_centre)
+        // tile centre as in psi.cu (psi_tile_centre: every staged x_j - c exact)
         const float a = xsm[i0], b = xsm[(i0 + T < n ? i0 + T : n) - 1], p = xsm[j0], q = xsm[j0 + jcount - 1];
-        bool swap = false;
-        const float c = psi_tile_centre(a, b, p, q, bi == bj, swap);
-        const bool wide = swap ? psi_tile_wide(p, q, a, q, s) : psi_tile_wide(a, b, a, q, s);
-        if (wide) swap = false;
-        const float cen = (PSI_CENTER && !wide) ? c : 0.f;
-        const int64_t ir = swap ? j0 : i0, is = swap ? i0 : j0;
-        const int scount = swap ? T : jcount;
+        const bool wide = psi_tile_wide(a, b, p, q, s);
+        const float cen = (PSI_CENTER && !wide) ? psi_tile_centre(a, q) : 0.f;
         __syncthreads();  // sx of the previous tile consumed
-        for (int k = tid; k < T; k += kPsiThreads) sx[k] = __fsub_rn((k < scount) ? xsm[is + k] : xpad, cen);
+        for (int k = tid; k < T; k += kPsiThreads) sx[k] = __fsub_rn((k < jcount) ? xsm[j0 + k] : xpad, cen);
         const double w = (bi == bj) ? 1.0 : 2.0;
         double tt;
         if (wide)  // see psi_tile_wide; out of line so the common path keeps its code and registers
-          tt = batch_wide_tile(pass, sx, xsm, n, ir, scount, s, xpad, w, red);
+          tt = batch_wide_tile(pass, sx, xsm, n, i0, jcount, s, xpad, w, red);
         else
-          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, ir, scount, s, xpad, w, red, cen)
-                           : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, ir, scount, s, xpad, w, red, cen);
+          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
+                           : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
         if (tid == 0) fx_add(acc, fx_from_double(tt));
       }
       if (tid == 0) finalize_pass(pass, fx_to_double(acc), n, &res);

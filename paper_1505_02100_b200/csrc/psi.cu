@@ -8,7 +8,7 @@
 // atomic counter.  Each thread keeps R rows i in registers and streams the tile's j values
 // from shared memory (one LDS.128 broadcast per 4 j); two pairs go through each packed
 // f32x2 instruction:
-//     u = fma(x'_j, s_i, -x'_i s_i)   (x' = x - c, c the tile's first row; s = fp32(1/g))
+//     u = fma(x'_j, s_i, -x'_i s_i)   (x' = x - c, c the tile centre; s = fp32(1/g))
 //     t = u*u   a = t*c + p_i   (c = fp32(-log2(e)/2), p_i in (-2, -1] a per-row phase)
 //     e = ex2.approx(a)   P6 = ((t - 15) t + 45) t - 15  |  P4 = (t - 6) t + 3  (exact integers)
 //     acc += P * e
@@ -17,16 +17,18 @@
 // the per-row phase p_i = -1 - frac(i * 0.618...) (24 random bits, a Weyl sequence)
 // dithers the SFU exp argument so the table-pattern bias of MUFU.EX2 averages to a
 // constant, and keeps |a| >= 1 (no input truncation inside MUFU); it is undone by scaling
-// each row's fp64 sum by 2^(-p_i) in fp64.  The per-row scale s_i = s + k_i ulp(s),
-// k_i in [-7, 7], decorrelates the fp32 rounding of u and t across rows (matters for
-// discretised samples with few distinct differences); it is a zero-mean dilation of
-// <= 1e-6 whose effect is second order.
+// each row's fp64 sum by 2^(-p_i) in fp64.  The antithetic per-row scale s_i = s + k_i ulp(s),
+// |k_i| <= 128, spreads the fp32 rounding of u, t, a and P(t) of repeated differences
+// (discretised samples) over 257 scales; its dilation cancels to first order between the two
+// rows of a pair (psi_tile.cuh).
 // fp32 accumulators hold 32 terms per lane (64 per row, PSI_CH), then go to per-row fp64; each tile's fp64
 // total is added as a 128-bit fixed-point integer, so the result does not depend on
 // tile scheduling, grid size or GPU count.
-// Wide tiles (rows spanning > 64 bandwidths, or values > 1000: outliers, tiny g) run difference
-// first with u^2 clamped so He_r cannot overflow (psi_tile_wide).  With a
-// PsiFin, the pass's last CTA runs its epilogue (Steps V / VII or Psi_r) instead of a launch.
+// The tile centre c makes every staged x_j - c exact (psi_tile_centre); the per-row scale is the
+// antithetic s + k_i ulp(s) of psi_tile.cuh.  Wide tiles (blocks spanning > 64 bandwidths, or
+// values > 1000: outliers, tiny g) run difference first with u^2 clamped so He_r cannot overflow
+// (psi_tile_wide).  With a PsiFin, the pass's last CTA runs its epilogue
+// (Steps V / VII or Psi_r) instead of a launch.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -81,33 +83,19 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       }
     }
     const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-    // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jcount - 1]]
-    // (off-diagonal row blocks are full: only the last block can be ragged, and it is diagonal)
-    int64_t ir = i0, is = j0;  // register-side block, staged block
-    int scount = jcount;
+    // tile centre (R >= 1, PSI_CENTER, not wide): psi_tile_centre makes every staged x_j - cen exact
     float cen = 0.f;
     bool wide = false;
     if constexpr (R > 0) {
+      // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jcount - 1]]
       const float a = __ldg(xs + i0), b = __ldg(xs + (i0 + T < n ? i0 + T : n) - 1);
       const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jcount - 1);
-      bool swap = false;
-      const float c = psi_tile_centre(a, b, p, q, bi == bj, swap);
-      wide = swap ? psi_tile_wide(p, q, a, q, s) : psi_tile_wide(a, b, a, q, s);
-      if (wide) {
-        swap = false;  // difference first: raw values, rows in registers
-      } else if (PSI_CENTER) {
-        cen = c;  // sx holds fl(x_j - cen), exact (psi_tile_centre)
-      }
-      if (swap) {  // the (full) row block is staged, the column block goes to registers
-        ir = j0;
-        is = i0;
-        scount = T;
-      }
+      wide = psi_tile_wide(a, b, p, q, s);
+      if (PSI_CENTER && !wide) cen = psi_tile_centre(a, q);
     }
-    // stage the tile's staged-block values: float4 loads (xs is 256-byte aligned, block starts are
-    // multiples of T)
-    if (scount == T) {
-      const float4* src = reinterpret_cast<const float4*>(xs + is);
+    // stage the tile's column values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
+    if (jcount == T) {
+      const float4* src = reinterpret_cast<const float4*>(xs + j0);
       float4* dst = reinterpret_cast<float4*>(sx);
       // T / 4 float4 per tile: one per thread for T >= 1024, the first T / 4 threads otherwise
       for (int q = tid; q < T / 4; q += kPsiThreads) {
@@ -119,15 +107,15 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
         dst[q] = v;
       }
     } else {
-      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < scount) ? __ldg(xs + is + q) : xpad, cen);
+      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + j0 + q) : xpad, cen);
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
     if constexpr (R == 0) {
       tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
     } else {
-      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, ir, scount, s, xpad, w, red);
-      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, ir, scount, s, xpad, w, red, cen);
+      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
     }
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
@@ -157,6 +145,8 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   ctrl->psi_done[slot] = 0u;
   finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
 }
+
+int64_t psi_work_units(int64_t n) { return n > 0 ? psi_tiles(n) : 0; }
 
 int psi_rows_per_thread(int64_t n) {
   if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2, 1; 0 = small tiles)

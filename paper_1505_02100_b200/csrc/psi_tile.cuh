@@ -16,6 +16,9 @@ namespace plg {
 #ifndef PSI_UNROLL
 #define PSI_UNROLL 16
 #endif
+#ifndef PSI_CENTER
+#define PSI_CENTER 1  // the centred FMA form of u; 0: difference first (A/B only)
+#endif
 constexpr int kPsiUnroll = PSI_UNROLL;
 
 // packed constants {v, v}
@@ -101,16 +104,17 @@ __device__ __forceinline__ u64 hermite_t(u64 t) {
 constexpr float kTClamp = 1024.f;  // a <= -0.7213 * 1024 - 1: ex2 -> +0
 // "wide" tiles take the variant psi_tile_sum<..., WIDE = true>: difference first and clamped,
 // inner loop rolled.  A tile is wide if its values span more than kClampSpan bandwidths
-// (otherwise |u| <= span * s and He_12(1000^2) < 1e37: no overflow), or its register-side block
-// spans more than kCenterSpan bandwidths (the centred form shifts each row by eps * |x_i - c| * s
-// in u: fine for a dense block, not for one that holds an outlier).  Both only
-// occur with outliers or a tiny g; none of the BASELINE configurations has such a tile.
+// (otherwise |u| <= span * s and He_12(1000^2) < 1e37: no overflow), or its row and column blocks
+// together span more than kCenterSpan bandwidths (the centred form shifts each row by
+// eps * |x_i - c| * s in u: fine for dense blocks, not for one that holds an
+// outlier).  Both only occur with outliers or a tiny g; none of the BASELINE configurations has
+// such a tile.
 constexpr double kClampSpan = 1000.0;
 constexpr double kCenterSpan = 64.0;
-// reg_lo/reg_hi: the register-side (row) block's values; lo/hi: the smallest and largest value of
-// the tile
-__device__ __forceinline__ bool psi_tile_wide(float reg_lo, float reg_hi, float lo, float hi, float s) {
-  return ((double)reg_hi - (double)reg_lo) * (double)s > kCenterSpan || ((double)hi - (double)lo) * (double)s > kClampSpan;
+// rows in [a, b], columns in [p, q] (sorted: a <= b <= p <= q)
+__device__ __forceinline__ bool psi_tile_wide(float a, float b, float p, float q, float s) {
+  return (((double)b - (double)a) + ((double)q - (double)p)) * (double)s > kCenterSpan ||
+         ((double)q - (double)a) * (double)s > kClampSpan;
 }
 
 // c rounded toward zero to a multiple of ulp(q), 0 <= c <= q (the grid is clamped to 2^-126: a
@@ -125,22 +129,18 @@ __device__ __forceinline__ float round_to_ulp_of(float c, float q) {
 // sorted sample (a <= b <= p <= q).  The centre c makes EVERY staged value fl(x_j - c) and every
 // row value fl(x_i - c) exact, so the only per-value roundings left are the dithered ones of
 // fl((x_i - c) s_i) and of the pair arithmetic (an inexact fl(x_j - c) is a fixed shift of a column
-// value shared by all 256 R rows of the tile: systematic on discretised samples):
+// value shared by all rows of the tile: systematic on discretised samples):
 //   all values >= 0: c = a, or, if some value exceeds 2a, a rounded toward 0 to a multiple of
 //     ulp(q): every x - c is then a multiple of ulp(x) no larger than x (or Sterbenz-exact);
-//   all values <= 0: the mirror image, c next to q, and the COLUMN block goes to registers
-//     (swap = true) so that |x_i - c| stays within one block;
-//   the tile spans 0: c = 0 (x - 0 is exact), with the block that holds 0 in registers.
-// The row side keeps |x_i - c| <= its block's span (+ ulp(q)), or <= |u| + span when 0 lies between
-// the blocks.  Diagonal tiles (one block) never swap.
-__device__ __forceinline__ float psi_tile_centre(float a, float b, float p, float q, bool diag, bool& swap) {
-  swap = false;
+//   all values <= 0: the mirror image, c = q (rounded toward 0 to a multiple of ulp(a));
+//   the tile spans 0: c = 0 (x - 0 is exact).
+// For every pair (i, j) of the tile |x_i - c| <= |x_j - x_i| + (b - a) + (q - p) (+ ulp(q)), so the
+// dithered rounding of fl((x_i - c) s_i) stays within eps (|u| + (b - a + q - p) s) of u: tiles whose
+// two blocks span more than kCenterSpan bandwidths together take the difference-first path
+// (psi_tile_wide).
+__device__ __forceinline__ float psi_tile_centre(float a, float q) {
   if (a >= 0.f) return (q <= 2.f * a) ? a : round_to_ulp_of(a, q);
-  if (q <= 0.f) {
-    swap = !diag;
-    return (a >= 2.f * q) ? q : -round_to_ulp_of(-q, -a);
-  }
-  swap = !diag && b < 0.f && p <= 0.f;
+  if (q <= 0.f) return (a >= 2.f * q) ? q : -round_to_ulp_of(-q, -a);
   return 0.f;
 }
 
@@ -227,10 +227,6 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
 //   xrows : the sorted sample, rows i0 .. i0 + T - 1 (i >= n reads as xpad and is dropped)
 //   red   : shared scratch of kPsiThreads / 32 doubles
 // Called by all 256 threads; the result is valid in thread 0.  Contains __syncthreads().
-#ifndef PSI_CENTER
-#define PSI_CENTER 1
-#endif
-
 // cen: the tile centre when PSI_CENTER (sx then holds fl(x_j - cen)); ignored otherwise
 // WIDE (psi_tile_wide): difference first (sx holds raw values, cen unused) and pair2's overflow
 // clamp; the inner loop stays rolled there to keep the code small.

@@ -13,7 +13,8 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("PLUGIN_LIB_PATH") or os.path.join(HERE, "libplugin.so")
+DEFAULT_LIB = os.path.join(HERE, "libplugin.so")
+LIB_PATH = os.environ.get("PLUGIN_LIB_PATH") or DEFAULT_LIB
 
 PLUGIN_OK, PLUGIN_E_INVALID, PLUGIN_E_NONFINITE, PLUGIN_E_DEGENERATE, PLUGIN_E_DOMAIN, PLUGIN_E_CUDA = range(6)
 STATUS_NAMES = {0: "PLUGIN_OK", 1: "PLUGIN_E_INVALID", 2: "PLUGIN_E_NONFINITE", 3: "PLUGIN_E_DEGENERATE",
@@ -85,6 +86,7 @@ def lib():
             "plugin_after_psi6": (i32, [P, P, P]),
             "plugin_after_psi4": (i32, [P, P, P]),
             "plugin_num_tiles": (i64, [i64]),
+            "plugin_tile_edge": (i64, [i64]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
             "plugin_sort": (i32, [P, i64, P, P, sz, P]),
@@ -99,6 +101,8 @@ def lib():
             "plugin_version": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
+            if LIB_PATH != DEFAULT_LIB and not hasattr(L, name):
+                continue  # an A/B variant library (PLUGIN_LIB_PATH) built from an older source
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
@@ -113,7 +117,7 @@ EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h",
             "plugin_graph_create", "plugin_graph_launch", "plugin_graph_destroy",
             "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
+            "plugin_shard_tiles", "plugin_tile_edge", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
             "kde_workspace_bytes", "kde_eval", "kde_prepare",
             "kde_eval_prepared", "plugin_last_error", "plugin_version")
 
@@ -350,6 +354,10 @@ def plugin_after_psi4(total: torch.Tensor, out: torch.Tensor, stream=None):
 
 def plugin_num_tiles(n: int) -> int:
     return lib().plugin_num_tiles(n)
+
+
+def plugin_tile_edge(n: int) -> int:
+    return lib().plugin_tile_edge(n)
 
 
 def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:

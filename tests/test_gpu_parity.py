@@ -213,10 +213,10 @@ def _tile_coords(t, nb):
     return b, b + (t - (b * nb - b * (b - 1) // 2))
 
 
-@pytest.mark.parametrize("k", [4, 5])
+@pytest.mark.parametrize("k", [3, 4, 5])
 def test_full_size_sampled_tile_shards(P, oracle_mod, k):
-    """Full-size configs in the launch configuration bench.py times: sampled tile ranges of
-    both passes (psi_r_shard, exact fixed-point partials) against the oracle's block sums of
+    """Full-size configs in the launch configuration bench.py times (cfg3: R = 4 tiles, cfg4/5:
+    R = 8): sampled tile ranges of both passes (psi_r_shard, exact fixed-point partials) against the oracle's block sums of
     the same pairs.  Bandwidths come from the oracle: g1 (Steps I-III, closed form) for r=6
     and 0.2 sigma for r=4 (the identity checked holds at any g)."""
     from paper_1505_02100_b200.distributed import from_limbs
@@ -233,11 +233,9 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
     res.status, res.n, res.g1, res.g2 = 0, n, g1, g4
     dres = torch.frombuffer(bytearray(bytes(res)), dtype=torch.uint8).cuda()
     zs = np.sort(oracle_mod.widen(x))
-    ntiles = P.plugin_num_tiles(n)
-    nb = int(round((-1 + math.sqrt(1 + 8 * ntiles)) / 2))
+    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
+    nb = -(-n // T)
     assert nb * (nb + 1) // 2 == ntiles
-    T = -(-n // nb)
-    T = next(t for t in (256, 512, 1024, 2048) if -(-n // t) == nb and t >= T)
     world = 1024
     phi0 = 1 / math.sqrt(2 * math.pi)
     for r, g in ((6, g1), (4, g4)):

@@ -80,6 +80,18 @@ int main(int argc, char** argv) {
       const int64_t jl = (j0 + T < n ? j0 + T : n) - 1;
       float cen = x[i0];
       int64_t ri0 = i0, rj0 = j0;
+      if (cmode == 6) {  // as 5, never swapping roles
+        const float a = x[i0], q = x[jl];
+        if (a >= 0.f) {
+          const float uq = nextafterf(q, INFINITY) - q;
+          cen = truncf(a / uq) * uq;
+        } else if (q <= 0.f) {
+          const float ua = nextafterf(-a, INFINITY) + a;
+          cen = truncf(q / ua) * ua;
+        } else {
+          cen = 0.f;
+        }
+      }
       if (cmode == 5) {
         const float a = x[i0], b = x[il], pp = x[j0], q = x[jl];
         if (a >= 0.f) {

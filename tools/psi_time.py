@@ -1,4 +1,5 @@
-"""Device time of the psi passes alone (psi_r_shard over all tiles, CUDA events, median of 20)
+"""Device time of the psi passes alone (psi_r_shard over all work items + its export kernel;
+CUDA events around 10 back-to-back calls, so the host-side call overhead overlaps; median of 20)
 at sizes n, N(0,1) samples, the bandwidths of Algorithm 1:
 python tools/psi_time.py 4096 16384 50000 ...   (PLUGIN_PSI_R / PLUGIN_PSI_WARP select tiles)"""
 import json
@@ -21,18 +22,21 @@ def main():
         ws = P.workspace(n, x.device)
         out = P.new_result(x.device)
         P.plugin_step1(x, out, ws)
-        row = {"n": n, "tiles": P.plugin_num_tiles(n)}
+        row = {"n": n, "units": P.plugin_num_tiles(n), "T": P.plugin_tile_edge(n),
+               "R_env": os.environ.get("PLUGIN_PSI_R", "")}
         for r in (6, 4):
             ts = []
+            part = P.new_partial(x.device)
+            reps = 10 if n < 200000 else 1
             for it in range(23):
-                part = P.new_partial(x.device)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                P.psi_r_shard(n, r, 0, 1, out, part, ws)
+                for _ in range(reps):
+                    P.psi_r_shard(n, r, 0, 1, out, part, ws)
                 e1.record()
                 torch.cuda.synchronize()
                 if it >= 3:
-                    ts.append(e0.elapsed_time(e1) * 1e3)
+                    ts.append(e0.elapsed_time(e1) * 1e3 / reps)
             (P.plugin_after_psi6 if r == 6 else P.plugin_after_psi4)(part, out)
             med = statistics.median(ts)
             row[f"psi{r}_us"] = round(med, 2)
