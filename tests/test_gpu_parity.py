@@ -52,6 +52,21 @@ def test_plugin_h_matches_oracle_on_baseline_configs(P, k):
         assert rel(r[key], g[key]) < TOL, (key, r[key], g[key], rel(r[key], g[key]))
 
 
+@pytest.mark.parametrize("name", list(inputs.ROUNDED))
+def test_plugin_h_matches_oracle_on_rounded_configs(P, name):
+    # BASELINE configs rounded to a grid (cfg4 to 0.01: n = 2^20 on 1631 distinct values,
+    # cancellation ~2e4 on psi6): golden values written by oracle.make_golden (oracle/ only)
+    p = os.path.join(HERE, "golden", f"cfg{name}.json")
+    with open(p) as f:
+        g = json.load(f)
+    x = inputs.rounded_data(name)
+    assert inputs.sha256_f32(x) == g["sha256"]
+    r = P.plugin_h_sync(torch.from_numpy(x).cuda())
+    assert r["status"] == 0
+    for key in ("psi6_z", "psi4_z", "h_z", "psi6", "psi4", "h", "g1", "g2", "sigma"):
+        assert rel(r[key], g[key]) < TOL, (key, r[key], g[key], rel(r[key], g[key]))
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 1023, 1025, 4097, 9000])
 @pytest.mark.parametrize("r", [4, 6])
 def test_psi_r_small_sweep(P, oracle_mod, n, r):
