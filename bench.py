@@ -33,8 +33,11 @@ sys.path.insert(0, ROOT)
 METRIC = "pairwise K4/K6 evaluations/sec (GPairs/s) and end-to-end h time vs FMA/SFU roofline, 1-8 GPUs"
 UNIT = "GPairs/s"
 MUFU_EX2_PER_CLK_PER_SM = 16      # measured: tools/probe/mufu_probe.cu (profiles/r01_mufu_probe.jsonl)
-KERNELS_PER_STEP = 19             # distributed API: 4 x (hist, scan, scatter), step1, 2 x (psi, export, finalize)
-KERNELS_PER_PLUGIN_H = 15         # plugin_h, n > 2048: 4 x 3 sort, step1, 2 x psi (finalize in its last CTA)
+# kernels of one step, n > 32768 (group.cu: from kGroupMinN = 32768 the distinct-value count and
+# compaction run after Step I, and each pass launches the fp32 tile pass and the grouped exact
+# pass, one of which returns at once)
+KERNELS_PER_STEP = 23             # distributed API: 12 radix sort, step1, 2 group, 2 x (psi, group psi, export, finalize)
+KERNELS_PER_PLUGIN_H = 19         # plugin_h: 12 radix sort, step1, 2 group, 2 x (psi, group psi) (finalize in the last CTA)
 
 
 def _args():
@@ -535,12 +538,12 @@ def run_variant(a):
         ws = torch.empty(P.lib().plugin_q32_workspace_bytes(n) + 256, dtype=torch.uint8, device=dev)
         ws = ws[(-ws.data_ptr()) % 256:][:P.lib().plugin_q32_workspace_bytes(n)]
         step = lambda: P.plugin_h_q32(x, out=out, ws=ws)  # noqa: E731
-        passes, launches = 2, 19    # 12 radix sort, Step I, encode, rg1, 2 x (pass, finalize)
+        passes, launches = 2, 21    # 12 radix sort, Step I, 2 group, encode, rg1, 2 x (pass, finalize)
     else:
         out = torch.empty(P.DPI_RESULT_BYTES, dtype=torch.uint8, device=dev)
         ws = P.workspace(n, dev)
         step = lambda: P.plugin_dpi(x, a.stages, out=out, ws=ws)  # noqa: E731
-        passes, launches = a.stages, 14 + 2 * a.stages  # 12 radix sort, Step I, init, l x (pass, finalize)
+        passes, launches = a.stages, 16 + 3 * a.stages  # 12 radix sort, Step I, 2 group, init, l x (pass, group pass, finalize)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(a.warmup):

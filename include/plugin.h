@@ -49,10 +49,13 @@ typedef enum {
   PLUGIN_E_CUDA = 5         /* a CUDA launch / copy failed (immediate)                   */
 } plugin_status;
 
+/* plugin_result.path bits: how the device evaluated the O(n^2) steps */
+#define PLUGIN_PATH_GROUPED 1  /* the exact fp64 pass over distinct values (heavily tied sample) */
+
 /* Written by the device.  Layout is part of the ABI (int32,int32,int64, then doubles). */
 typedef struct {
   int32_t status;     /* plugin_status of the data-dependent checks                          */
-  int32_t reserved;
+  int32_t path;       /* PLUGIN_PATH_* bits (plugin_h / psi_r; 0 from the multi-GPU calls)   */
   int64_t n;
   double mean;        /* Step I: sample mean                                       */
   double var;         /* Step I: V = sum X^2/(n-1) - (sum X)^2/(n(n-1)) (evaluated shifted)   */
@@ -157,7 +160,8 @@ plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
 
 /* One rank's share of a psi pass (Steps IV/VI, Eq. 6/7):
  * the tiles [w*rank/world, w*(rank+1)/world) of the pair triangle (w = plugin_num_tiles(n)),
- * at the bandwidth of d_out (g1 for r=6, g2 for r=4), written as an unnormalised fixed-point
+ * at the bandwidth of d_out (g1 for r=6, g2 for r=4 -- and g2 for the other even r <= 12 of
+ * the plugin_dpi family, K^(r) = He_r phi), written as an unnormalised fixed-point
  * sum to *d_partial.  The tiles partition the pairs (sorted sample, upper block triangle,
  * diagonal tiles as full squares) identically for every world, and sums are exact integers:
  * any world gives the single-GPU bits.

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libplugin.so")
-SOURCES = ["abi.cu", "scalar.cu", "sort.cu", "psi.cu", "kde.cu", "fused.cu", "dpi.cu", "q32.cu"]
+SOURCES = ["abi.cu", "scalar.cu", "sort.cu", "psi.cu", "group.cu", "kde.cu", "fused.cu", "dpi.cu", "q32.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xptxas", "-v"]

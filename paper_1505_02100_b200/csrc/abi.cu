@@ -42,6 +42,14 @@ Layout layout(int64_t n) {
   off = align_up(off + sizeof(plugin_result), 256);
   L.fused = off;
   off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid + 256, 256);  // fused.cu partials (32 KB) + timing slots
+  // group.cu: per-4096-chunk distinct counts, then at most n/4 distinct values and run starts (+1)
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  L.grp_heads = off;
+  off = align_up(off + sizeof(unsigned int) * (nn / 4096 + 1), 256);
+  L.grp_v = off;
+  off = align_up(off + sizeof(float) * (nn / 4 + 1), 256);
+  L.grp_s = off;
+  off = align_up(off + sizeof(int) * (nn / 4 + 2), 256);
   L.total = off;
   return L;
 }
@@ -53,6 +61,9 @@ struct WS {
   float* xs;
   unsigned int* tmp;
   unsigned int* hist;
+  unsigned int* grp_heads;
+  float* grp_v;
+  int* grp_s;
 };
 
 static plugin_status get_ws(void* d_ws, size_t ws_bytes, int64_t n, WS& w) {
@@ -67,6 +78,9 @@ static plugin_status get_ws(void* d_ws, size_t ws_bytes, int64_t n, WS& w) {
   w.xs = reinterpret_cast<float*>(b + w.L.xs);
   w.tmp = reinterpret_cast<unsigned int*>(b + w.L.tmp);
   w.hist = reinterpret_cast<unsigned int*>(b + w.L.hist);
+  w.grp_heads = reinterpret_cast<unsigned int*>(b + w.L.grp_heads);
+  w.grp_v = reinterpret_cast<float*>(b + w.L.grp_v);
+  w.grp_s = reinterpret_cast<int*>(b + w.L.grp_s);
   return PLUGIN_OK;
 }
 
@@ -84,7 +98,21 @@ static plugin_status run_step1(const float* d_x, int64_t n, plugin_result* d_out
   // multiset of X only (bit-identical under any permutation of the input)
   if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, d_out, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  // heavily tied samples: the passes run grouped by distinct value, exactly (group.cu)
+  if ((e = launch_group_build(w.xs, n, w.ctrl, w.grp_heads, w.grp_v, w.grp_s, d_out, s)) != cudaSuccess)
+    return cuda_fail(e, "group");
   return PLUGIN_OK;
+}
+
+// one pass over all of the pair triangle (or a rank's share): the fp32 tile pass and the grouped
+// exact pass are both launched; the device runs the one ctrl->grouped selects
+static cudaError_t pass(WS& w, int64_t n, int r, int skip, double g_host, const double* g_dev, const int32_t* status_dev,
+                        int slot, int rank, int world, cudaStream_t s, PsiFin fin) {
+  const int64_t tiles = psi_work_units(n);
+  cudaError_t e = launch_psi(w.xs, n, r, skip, g_host, g_dev, status_dev, w.ctrl, slot, tiles * rank / world,
+                             tiles * (rank + 1) / world, s, fin);
+  if (e != cudaSuccess) return e;
+  return launch_group_psi(n, r, g_host, g_dev, status_dev, w.ctrl, slot, rank, world, w.grp_v, w.grp_s, s, fin);
 }
 
 }  // namespace plg
@@ -144,14 +172,13 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
     (void)cudaGetLastError();  // not applicable here: take the multi-kernel path
   }
   if ((st = run_step1(d_x, n, d_out, w, s)) != PLUGIN_OK) return st;
-  const int64_t tiles = psi_work_units(n);
   // each pass finalises itself in its last CTA (Steps V / VII; PsiFin)
   PsiFin f6, f4;
   f6.what = 0, f6.out = d_out, f6.r = 6;
   f4.what = 1, f4.out = d_out, f4.r = 4;
-  if ((e = launch_psi(w.xs, n, 6, skip, 0.0, &d_out->g1, &d_out->status, w.ctrl, 0, 0, tiles, s, f6)) != cudaSuccess)
+  if ((e = pass(w, n, 6, skip, 0.0, &d_out->g1, &d_out->status, 0, 0, 1, s, f6)) != cudaSuccess)
     return cuda_fail(e, "psi6");
-  if ((e = launch_psi(w.xs, n, 4, skip, 0.0, &d_out->g2, &d_out->status, w.ctrl, 1, 0, tiles, s, f4)) != cudaSuccess)
+  if ((e = pass(w, n, 4, skip, 0.0, &d_out->g2, &d_out->status, 1, 0, 1, s, f4)) != cudaSuccess)
     return cuda_fail(e, "psi4");
   return PLUGIN_OK;
 }
@@ -209,13 +236,15 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
   cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
   if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
   if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
-  // Step I reduction only for its non-finite flag (a NaN/Inf sample makes Psi NaN)
+  // Step I reduction only for its non-finite flag (a NaN/Inf sample makes Psi NaN); the distinct
+  // count for the grouped exact pass
   plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
   if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  if ((e = launch_group_build(w.xs, n, w.ctrl, w.grp_heads, w.grp_v, w.grp_s, scratch, s)) != cudaSuccess)
+    return cuda_fail(e, "group");
   PsiFin fin;  // Psi_r(g) written by the pass's last CTA
   fin.what = 2, fin.g = g, fin.r = r, fin.d_psi = d_psi;
-  if ((e = launch_psi(w.xs, n, r, 0, g, nullptr, nullptr, w.ctrl, 1, 0, psi_work_units(n), s, fin)) != cudaSuccess)
-    return cuda_fail(e, "psi");
+  if ((e = pass(w, n, r, 0, g, nullptr, nullptr, 1, 0, 1, s, fin)) != cudaSuccess) return cuda_fail(e, "psi");
   return PLUGIN_OK;
 }
 
@@ -236,16 +265,14 @@ plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_re
   if (!d_out || !d_partial) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
   plugin_status st = check_n(n, 2);
   if (st != PLUGIN_OK) return st;
-  if (r != 4 && r != 6) return fail(PLUGIN_E_INVALID, "r must be 4 or 6%s (r=%lld)", "", r);
+  if (r < 0 || r > 12 || (r & 1)) return fail(PLUGIN_E_INVALID, "r must be even, 0..12%s (r=%lld)", "", r);
   if (world < 1 || rank < 0 || rank >= world) return fail(PLUGIN_E_INVALID, "bad rank/world%s");
   WS w;
   if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
-  int64_t tb, te;
-  plugin_shard_tiles(n, rank, world, &tb, &te);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int slot = (r == 6) ? 0 : 1;
-  cudaError_t e = launch_psi(w.xs, n, r, 0, 0.0, r == 6 ? &d_out->g1 : &d_out->g2, &d_out->status, w.ctrl, slot,
-                             tb, te, s);
+  cudaError_t e = pass(w, n, r, 0, 0.0, r == 6 ? &d_out->g1 : &d_out->g2, &d_out->status, slot, rank, world, s,
+                       PsiFin());
   if (e != cudaSuccess) return cuda_fail(e, "psi shard");
   if ((e = launch_finalize(3, w.ctrl, slot, nullptr, nullptr, n, 0.0, r, nullptr, d_partial, s)) != cudaSuccess)
     return cuda_fail(e, "export partial");
@@ -366,10 +393,9 @@ plugin_status plugin_dpi(const float* d_x, int64_t n, int stages, plugin_dpi_res
   if ((st = run_step1(d_x, n, s1, w, s)) != PLUGIN_OK) return st;
   cudaError_t e;
   if ((e = launch_dpi_init(s1, stages, d_out, s)) != cudaSuccess) return cuda_fail(e, "dpi init");
-  const int64_t tiles = psi_work_units(n);
   for (int j = stages; j >= 1; --j) {
     const int slot = j & 1;
-    if ((e = launch_psi(w.xs, n, 2 * j + 2, 0, 0.0, &d_out->g[j - 1], &d_out->status, w.ctrl, slot, 0, tiles, s)) !=
+    if ((e = pass(w, n, 2 * j + 2, 0, 0.0, &d_out->g[j - 1], &d_out->status, slot, 0, 1, s, PsiFin())) !=
         cudaSuccess)
       return cuda_fail(e, "dpi pass");
     if ((e = launch_dpi_finalize(w.ctrl, slot, j, d_out, s)) != cudaSuccess) return cuda_fail(e, "dpi finalize");

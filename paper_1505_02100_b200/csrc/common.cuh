@@ -35,6 +35,10 @@ inline __host__ __device__ int step1_grid(int64_t n) {
 }
 // the fused single-launch path (fused.cu) handles n up to this
 constexpr int64_t kFusedMaxN = 2048;
+// the grouped exact pass (group.cu) is considered from this n on, for samples with at most n / 4
+// distinct values; below it the fp32 pass meets 1e-5 on the discretised test samples
+// and the extra launches would weigh on the latency
+constexpr int64_t kGroupMinN = 32768;
 
 // rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
 int psi_rows_per_thread(int64_t n);
@@ -67,12 +71,15 @@ struct Ctrl {                       // zeroed at the start of every API call
   unsigned int step1_done;          // last-block-done counter of Step I
   int nonfinite;                    // set if any X is NaN/Inf
   unsigned int psi_done[2];         // last-CTA-done counters of the psi passes (PsiFin)
-  unsigned int pad[54];
+  long long distinct;               // number of distinct values of the sample (group.cu)
+  int grouped;                      // 1: the passes run grouped by distinct value in fp64 (group.cu)
+  unsigned int group_done;          // last-CTA-done counter of group_count_kernel
+  unsigned int pad[50];
 };
 static_assert(sizeof(Ctrl) <= 512, "ctrl block");
 
 struct Layout {
-  size_t ctrl, step1, xs, tmp, hist, result, fused, total;
+  size_t ctrl, step1, xs, tmp, hist, result, fused, grp_heads, grp_v, grp_s, total;
   int64_t sort_blocks;
 };
 Layout layout(int64_t n);
@@ -149,6 +156,13 @@ cudaError_t launch_q32_rg1(const plugin_result* res, long long* rg, cudaStream_t
 constexpr int kDpiMaxStages = PLUGIN_DPI_MAX_STAGES;
 cudaError_t launch_dpi_init(const plugin_result* s1, int stages, plugin_dpi_result* out, cudaStream_t s);
 cudaError_t launch_dpi_finalize(Ctrl* ctrl, int slot, int j, plugin_dpi_result* out, cudaStream_t s);
+// the grouped exact pass (group.cu): count the distinct values of the sorted copy and decide
+// (ctrl->grouped), compact them (gv values, gs run starts with gs[m] = n); then per pass
+cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned int* chunk_heads, float* gv, int* gs,
+                               const plugin_result* s1, cudaStream_t s);
+cudaError_t launch_group_psi(int64_t n, int r, double g_host, const double* g_dev, const int32_t* status_dev,
+                             Ctrl* ctrl, int slot, int rank, int world, const float* gv, const int* gs, cudaStream_t s,
+                             PsiFin fin = PsiFin());
 // KDE of Eq. 1-2 at m points over the sorted sample xs (kde.cu); `extra` holds
 // kde_extra_bytes(n, m) bytes of workspace
 size_t kde_extra_bytes(int64_t n, int64_t m);

@@ -37,9 +37,13 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
   return r;
 }
 __device__ __forceinline__ float ex2(float a) {
+#ifdef PSI_EX2_EXACT  // A/B probe only: the correctly rounded 2^a (fp64), +0 below 2^-126 as ftz
+  return a < -126.f ? 0.f : __double2float_rn(exp2((double)a));
+#else
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
   return r;
+#endif
 }
 
 // float -> double on the integer (ALU) pipe.  cvt.f64.f32 (F2F) issues on the XU pipe,

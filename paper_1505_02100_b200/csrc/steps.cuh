@@ -134,7 +134,7 @@ __device__ __forceinline__ void finalize_total(int what, Fx128 acc, bool nonfini
 __device__ __forceinline__ void init_result(plugin_result* out, int64_t n) {
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   out->status = PLUGIN_OK;
-  out->reserved = 0;
+  out->path = 0;
   out->n = n;
   double* f = &out->mean;
   const int nf = (int)((sizeof(plugin_result) - offsetof(plugin_result, mean)) / sizeof(double));

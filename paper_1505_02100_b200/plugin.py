@@ -28,12 +28,12 @@ class PluginError(RuntimeError):
 
 
 class plugin_result(ctypes.Structure):
-    _fields_ = [("status", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n", ctypes.c_int64)] + [
+    _fields_ = [("status", ctypes.c_int32), ("path", ctypes.c_int32), ("n", ctypes.c_int64)] + [
         (k, ctypes.c_double) for k in ("mean", "var", "sigma", "psi8_ns", "g1", "psi6", "g2", "psi4", "h",
                                        "g1_z", "psi6_z", "g2_z", "psi4_z", "h_z", "S6", "S4")]
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 DPI_MAX_STAGES = 5
@@ -112,6 +112,7 @@ def lib():
 
 PLUGIN_SKIP_UNDERFLOW = 1
 PLUGIN_MULTI_KERNEL = 2
+PLUGIN_PATH_GROUPED = 1  # plugin_result["path"] bit: the exact grouped fp64 pass ran (group.cu)
 
 EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h", "plugin_h_ex", "plugin_h_batch",
             "plugin_graph_create", "plugin_graph_launch", "plugin_graph_destroy",

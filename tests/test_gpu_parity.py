@@ -568,3 +568,78 @@ def test_plugin_h_on_a_second_device(P):
     a = P.plugin_h_sync(torch.from_numpy(x).to("cuda:0"))
     b = P.plugin_h_sync(torch.from_numpy(x).to("cuda:1"))
     assert _same(a, b)
+
+
+def _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb):
+    bi, bj = _tile_coords(t, nb)
+    rows = (bi * T, min(n, bi * T + T))
+    cols = (bj * T, min(n, bj * T + T))
+    w = 1.0 if bi == bj else 2.0
+    return w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols)
+
+
+def _one_tile(P, n, r, t, ntiles, dres, ws):
+    """The exact fixed-point sum of tile t alone (psi_r_shard with one tile per 'rank')."""
+    from paper_1505_02100_b200.distributed import from_limbs
+    part = P.new_partial()
+    P.psi_r_shard(n, r, t, ntiles, dres, part, ws)
+    assert P.plugin_shard_tiles(n, t, ntiles) == (t, t + 1)
+    return from_limbs(part.cpu().tolist()) / 2.0 ** 64 / math.sqrt(2 * math.pi)
+
+
+def _bandwidth_record(P, n, g_a, g_b):
+    res = P.plugin_result()
+    res.status, res.n, res.g1, res.g2 = 0, n, g_a, g_b
+    return torch.frombuffer(bytearray(bytes(res)), dtype=torch.uint8).cuda()
+
+
+@pytest.mark.parametrize("n", [100000, 300000])
+def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
+    """Outliers at the sizes that select R = 4 (n = 1e5, T = 1024) and R = 8 (n = 3e5, T = 2048)
+    tiles: the tiles that hold them span far more than 64 bandwidths and take the wide path
+    (difference first, clamped u^2, psi_tile.cuh); those tiles, the diagonal tiles at both ends and
+    a middle tile, one by one against the oracle's block sums of the same pairs."""
+    rng = np.random.default_rng(50 + n)
+    far = np.array([3e3, -5e3, 1e5, 1e7, -2e4, 40.0, -60.0], dtype=np.float32)
+    x = np.concatenate([rng.normal(0, 1, n - far.size).astype(np.float32), far])
+    x = x[rng.permutation(n)]
+    xd = torch.from_numpy(x).cuda()
+    ws = P.workspace(n)
+    P.plugin_step1(xd, P.new_result(), ws)
+    zs = np.sort(oracle_mod.widen(x))
+    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
+    assert T == (1024 if n == 100000 else 2048)
+    nb = -(-n // T)
+    picks = sorted({0, 1, nb - 1, nb // 2 * nb - (nb // 2) * (nb // 2 - 1) // 2,   # row 0 (outliers), mid diag
+                    ntiles - 1, ntiles - 2,                                           # last tiles
+                    (nb - 2) * nb - (nb - 2) * (nb - 3) // 2 + 1})                    # row nb-2, last column
+    for r, g in ((6, 0.3), (4, 0.2)):
+        dres = _bandwidth_record(P, n, g, g)
+        for t in picks:
+            got = _one_tile(P, n, r, t, ntiles, dres, ws)
+            ref = _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb)
+            assert math.isfinite(got)
+            # relative 1e-5; terms below the fp32 range (e^(-u^2/2) < 2^-126: the far tiles) are
+            # +0 on the GPU, so an absolute T^2 2^-100 is allowed on top
+            assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (n, r, t, _tile_coords(t, nb), got, ref)
+
+
+@pytest.mark.parametrize("r", [8, 12])
+def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
+    """The general-r pass (He_r phi, the plugin_dpi family) at BASELINE config 4 (R = 8 tiles,
+    where test_gpu_dpi's full-oracle cases do not reach): sampled tiles against the oracle."""
+    x = inputs.config_data(4)
+    n = x.size
+    xd = torch.from_numpy(x).cuda()
+    ws = P.workspace(n)
+    P.plugin_step1(xd, P.new_result(), ws)
+    zs = np.sort(oracle_mod.widen(x))
+    sigma = oracle_mod.step1(x)["sigma"]
+    g = 0.35 * sigma
+    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
+    nb = -(-n // T)
+    dres = _bandwidth_record(P, n, g, g)
+    for t in (0, 5, nb + 3, ntiles // 2, ntiles // 2 + 1, ntiles - 3, ntiles - 1):
+        got = _one_tile(P, n, r, t, ntiles, dres, ws)
+        ref = _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb)
+        assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, _tile_coords(t, nb), got, ref)

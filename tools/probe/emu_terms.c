@@ -60,7 +60,8 @@ int main(int argc, char** argv) {
   int flags = atoi(argv[6]);
   int variant = argc > 7 ? atoi(argv[7]) : 0;
   if (argc > 8) g_anti = atoi(argv[8]);
-  int cmode = argc > 9 ? atoi(argv[9]) : 0;  // tile centre: 0 x[i0], 1 x[i0] + random part of the row span, 2 zero, 3 difference first
+  int cmode = argc > 9 ? atoi(argv[9]) : 0;
+  int stride = argc > 10 ? atoi(argv[10]) : 1;  // evaluate rows i % stride == 0 only (sampled)  // tile centre: 0 x[i0], 1 x[i0] + random part of the row span, 2 zero, 3 difference first
   float* x = malloc(n * 4);
   if (fread(x, 4, n, f) != (size_t)n) return 2;
   fclose(f);
@@ -70,14 +71,31 @@ int main(int argc, char** argv) {
   const float sf = f32(1.0 / g);
   int64_t nb = (n + T - 1) / T;
   double total = 0.0, comp = 0.0;
+  const char* tb_env = getenv("EMU_TILE_BI");  // restrict to one tile (bi, bj)
+  const int64_t only_bi = tb_env ? atoll(tb_env) : -1, only_bj = tb_env ? atoll(getenv("EMU_TILE_BJ")) : -1;
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : total)
   for (int64_t bi = 0; bi < nb; ++bi) {
     double tot_b = 0.0;
+    if (only_bi >= 0 && bi != only_bi) continue;
     for (int64_t bj = bi; bj < nb; ++bj) {
+      if (only_bj >= 0 && bj != only_bj) continue;
       const int64_t i0 = bi * T, j0 = bj * T;
       const double w = (bi == bj) ? 1.0 : 2.0;
       float cen = x[i0];
       int64_t ri0 = i0, rj0 = j0;  // register-side block, staged block
+      if (cmode == 6) {  // the kernel's rule (psi_tile_centre), rows always in registers
+        const int64_t jl = (j0 + T < n ? j0 + T : n) - 1;
+        const float a = x[i0], q = x[jl];
+        if (a >= 0.f) {
+          const float uq = nextafterf(q, INFINITY) - q;
+          cen = (q <= 2.f * a) ? a : truncf(a / uq) * uq;
+        } else if (q <= 0.f) {
+          const float ua = nextafterf(-a, INFINITY) + a;
+          cen = (a >= 2.f * q) ? q : truncf(q / ua) * ua;
+        } else {
+          cen = 0.f;
+        }
+      }
       if (cmode == 5) {
         const int64_t il = (i0 + T < n ? i0 + T : n) - 1;
         const int64_t jl = (j0 + T < n ? j0 + T : n) - 1;
@@ -118,9 +136,13 @@ int main(int argc, char** argv) {
       }
       double tile = 0.0;
       for (int64_t i = ri0; i < ri0 + T && i < n; ++i) {
+        if (stride > 1 && ((i >> 1) % (stride >> 1)) != 0) continue;  // keep antithetic row pairs whole
         double si;
         float sif = sf;
-        if (flags & 1) sif = u2f(f2u(sf) + (g_anti ? anti_offset(i) : row_scale_offset(i)));
+        if (flags & 1) {
+          const float ulps = u2f((f2u(sf) & 0x7f800000u) - (23u << 23));
+          sif = g_anti ? fmaf((float)anti_offset(i), ulps, sf) : u2f(f2u(sf) + row_scale_offset(i));
+        }
         si = (flags & (1 | 2)) ? (double)sif : 1.0 / g;
         const float p = row_phase(i);
         const float xi_c = x[i] - cen;  // fl(x_i - c)

@@ -57,9 +57,10 @@ def main():
                "lib": os.path.basename(P.LIB_PATH)}
         if hasattr(P.lib(), "plugin_tile_edge"):
             row["T"] = P.plugin_tile_edge(n)
-        # an empty shard (rank with no work) runs only the export kernel
+        # an empty shard (rank 0 of units + 1 ranks owns [0, 0)) runs only the export kernel
         world = P.plugin_num_tiles(n) + 1
-        export = graph_us(lambda: P.psi_r_shard(n, 6, world - 1, world, out, part, ws))
+        assert P.plugin_shard_tiles(n, 0, world) == (0, 0)
+        export = graph_us(lambda: P.psi_r_shard(n, 6, 0, world, out, part, ws))
         row["export_us"] = round(export, 2)
         pairs = n * (n - 1) / 2
         for r in (6, 4):
