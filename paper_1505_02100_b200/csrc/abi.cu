@@ -131,6 +131,11 @@ int64_t plugin_num_tiles(int64_t n) { return n > 0 ? psi_work_units(n) : 0; }
 
 int64_t plugin_tile_edge(int64_t n) { return n > 0 ? psi_tile_edge(n) : 0; }
 
+int plugin_work_item(int64_t n, int64_t item, int64_t* out5) {
+  if (!out5) return -1;
+  return psi_work_item(n, item, out5) ? 0 : -1;
+}
+
 void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end) {
   int64_t w = plugin_num_tiles(n);
   if (world < 1 || rank < 0 || rank >= world) {

@@ -49,9 +49,14 @@ inline int64_t psi_tile_edge(int64_t n) {
 }
 inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
-// the pass's schedulable work items for n samples (a function of n only): its tiles; launch_psi
-// ranges and the multi-GPU shards (plugin_shard_tiles) count these
+// the pass's schedulable work items for n samples (a function of n only): whole tiles, then the
+// column quarters of the tail tiles (psi.cu); launch_psi ranges and the multi-GPU shards
+// (plugin_shard_tiles) count these.  psi_work_item: rows [out0, out1), columns [out2, out3) and
+// weight out4 of one item (host)
+constexpr int kTailSplit = 4;
 int64_t psi_work_units(int64_t n);
+int64_t psi_tail_head(int64_t n);
+bool psi_work_item(int64_t n, int64_t item, int64_t* out);
 
 // order-preserving float bits <-> uint32 radix key (sort.cu, fused.cu)
 __device__ __forceinline__ unsigned int bits2key(unsigned int b) {
@@ -116,7 +121,8 @@ cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials
                          cudaStream_t s);
 cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp, unsigned int* hist,
                         int64_t nblocks, cudaStream_t s);
-// One pass of Steps IV/VI (or Psi_r for any even r <= 12) over tiles [tile_begin, tile_end):
+// One pass of Steps IV/VI (or Psi_r for any even r <= 12) over work items [tile_begin, tile_end)
+// (psi_work_units):
 // g from *g_dev (a device bandwidth; the pass is skipped unless *status_dev == PLUGIN_OK) or,
 // if g_dev is null, g_host.  skip != 0: skip tiles whose terms are all exactly 0 (NEXT 4).
 // The pass's epilogue, run by its last CTA to finish (saves the finalize launch): what = -1

@@ -37,14 +37,18 @@
 
 namespace plg {
 
-// min resident CTAs per SM for the register budget: R=8 -> 2 (<=128 regs), R<=4 -> 3 (<=80 regs)
+// min resident CTAs per SM for the register budget: R=8 -> 2 (<=128 regs), R=4 -> 3 (<=80 regs), R<=2 -> 4 (<=64)
+#ifndef PSI_OCC_R12
+#define PSI_OCC_R12 4  // R = 1, 2: <= 64 registers, no spills; 1-3% over 3 CTAs/SM at n = 12K..65K (profiles/r02p_ab_occ.jsonl)
+#endif
 template <int R>
-struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R == 0 ? 4 : 3); };
+struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R == 0 ? 4 : (R <= 2 ? PSI_OCC_R12 : 3)); };
 
 template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
-           const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, PsiFin fin) {
+           const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, int64_t head,
+           PsiFin fin) {
   constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
@@ -68,8 +72,18 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   for (;;) {
     if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
     __syncthreads();
-    const int64_t t = s_tile;
-    if (t >= tile_end) break;
+    const int64_t item = s_tile;
+    if (item >= tile_end) break;
+    // work item -> tile t and its column range [k0, k0 + kw): items < head are whole tiles, the
+    // rest are column quarters of the tail tiles (psi_tail_head)
+    int64_t t = item;
+    int k0 = 0, kw = T;
+    if (item >= head) {
+      const int64_t qq = item - head;
+      t = head + qq / kTailSplit;
+      kw = T / kTailSplit;
+      k0 = (int)(qq % kTailSplit) * kw;
+    }
     int64_t bi, bj;
     tile_coords(t, nb, bi, bj);
     const int64_t i0 = bi * T, j0 = bj * T;
@@ -84,23 +98,30 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
         continue;
       }
     }
-    const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-    // tile centre (R >= 1, PSI_CENTER, not wide): psi_tile_centre makes every staged x_j - cen exact
+    const int jtile = (int)((n - j0) < T ? (n - j0) : T);  // real columns of the tile
+    const int jcount = jtile - k0 < kw ? (jtile - k0 > 0 ? jtile - k0 : 0) : kw;  // ... of this item
+    if (jcount == 0) {  // a quarter past the sample's end (ragged last column block): no pairs
+      __syncthreads();
+      continue;
+    }
+    // tile centre (R >= 1, PSI_CENTER, not wide): psi_tile_centre makes every staged x_j - cen
+    // exact; decided on the whole tile, so the quarters of a tile agree
     float cen = 0.f;
     bool wide = false;
     if constexpr (R > 0) {
-      // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jcount - 1]]
+      // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jtile - 1]]
       const float a = __ldg(xs + i0), b = __ldg(xs + (i0 + T < n ? i0 + T : n) - 1);
-      const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jcount - 1);
+      const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jtile - 1);
       wide = psi_tile_wide(a, b, p, q, s);
       if (PSI_CENTER && !wide) cen = psi_tile_centre(a, q);
     }
-    // stage the tile's column values: float4 loads (xs is 256-byte aligned, j0 a multiple of T)
-    if (jcount == T) {
-      const float4* src = reinterpret_cast<const float4*>(xs + j0);
+    const int64_t jb = j0 + k0;  // first staged column
+    // stage the item's column values: float4 loads (xs is 256-byte aligned, jb a multiple of 64)
+    if (jcount == kw) {
+      const float4* src = reinterpret_cast<const float4*>(xs + jb);
       float4* dst = reinterpret_cast<float4*>(sx);
-      // T / 4 float4 per tile: one per thread for T >= 1024, the first T / 4 threads otherwise
-      for (int q = tid; q < T / 4; q += kPsiThreads) {
+      // kw / 4 float4: one per thread for kw >= 1024, the first kw / 4 threads otherwise
+      for (int q = tid; q < kw / 4; q += kPsiThreads) {
         float4 v = __ldg(src + q);
         v.x = __fsub_rn(v.x, cen);  // cen = 0 (exact no-op) for the small tiles of R = 0
         v.y = __fsub_rn(v.y, cen);
@@ -109,7 +130,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
         dst[q] = v;
       }
     } else {
-      for (int q = tid; q < T; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + j0 + q) : xpad, cen);
+      for (int q = tid; q < kw; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + jb + q) : xpad, cen);
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
@@ -148,7 +169,53 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
 }
 
-int64_t psi_work_units(int64_t n) { return n > 0 ? psi_tiles(n) : 0; }
+// resident CTAs of a B200 (148 SMs) at the occupancy the kernel is built for
+static int64_t psi_ref_slots(int R) { return 148LL * (R >= 8 ? 2 : (R <= 2 ? PSI_OCC_R12 : 3)); }
+
+// Tail split (A/B option, off by default): the last S + (tiles mod S) tiles (S = resident CTAs
+// of a B200) cut into kTailSplit column quarters so a pass would end on fine items.  Measured
+// (profiles/r02o_ab_tail.jsonl, CUDA graphs): 7-11% slower at n = 8K..25K (the per-item setup of
+// 4x more items outweighs the shorter tail), +3% at 64K, within 1% from 128K; so items are whole
+// tiles unless PLUGIN_PSI_TAIL=1.  A function of n (and that switch) only.  Items [0, head) are
+// whole tiles.
+int64_t psi_tail_head(int64_t n) {
+  const int64_t tiles = psi_tiles(n);
+  const int R = psi_rows_per_thread(n);
+  if (R == 0) return tiles;
+  const char* e = getenv("PLUGIN_PSI_TAIL");
+  if (!e || e[0] != '1') return tiles;
+  const int64_t S = psi_ref_slots(R);
+  const int64_t tail = S + tiles % S;
+  return tiles > tail ? tiles - tail : 0;
+}
+
+int64_t psi_work_units(int64_t n) {
+  if (n <= 0) return 0;
+  const int64_t tiles = psi_tiles(n), head = psi_tail_head(n);
+  return head + kTailSplit * (tiles - head);
+}
+
+bool psi_work_item(int64_t n, int64_t item, int64_t* out) {
+  if (n <= 0 || item < 0 || item >= psi_work_units(n)) return false;
+  const int64_t T = psi_tile_edge(n), nb = (n + T - 1) / T, head = psi_tail_head(n);
+  int64_t t = item, k0 = 0, kw = T;
+  if (item >= head) {
+    t = head + (item - head) / kTailSplit;
+    kw = T / kTailSplit;
+    k0 = ((item - head) % kTailSplit) * kw;
+  }
+  // row-major upper block triangle incl. the diagonal (as tile_coords)
+  int64_t b = 0;
+  while (b + 1 < nb && (b + 1) * nb - (b + 1) * b / 2 <= t) ++b;
+  const int64_t bj = b + (t - (b * nb - b * (b - 1) / 2));
+  out[0] = b * T;
+  out[1] = (b * T + T < n) ? b * T + T : n;
+  out[2] = bj * T + k0;
+  out[3] = (bj * T + k0 + kw < n) ? bj * T + k0 + kw : n;
+  if (out[3] < out[2]) out[3] = out[2];
+  out[4] = (b == bj) ? 1 : 2;
+  return true;
+}
 
 int psi_rows_per_thread(int64_t n) {
   if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2, 1; 0 = small tiles)
@@ -182,7 +249,8 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   int64_t tiles = te - tb;
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;
-  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, fin);
+  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te,
+                                                   psi_tail_head(n), fin);
   return cudaGetLastError();
 }
 

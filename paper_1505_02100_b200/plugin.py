@@ -87,6 +87,7 @@ def lib():
             "plugin_after_psi4": (i32, [P, P, P]),
             "plugin_num_tiles": (i64, [i64]),
             "plugin_tile_edge": (i64, [i64]),
+            "plugin_work_item": (i32, [i64, i64, ctypes.POINTER(i64)]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
             "plugin_sort": (i32, [P, i64, P, P, sz, P]),
@@ -118,7 +119,7 @@ EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h",
             "plugin_graph_create", "plugin_graph_launch", "plugin_graph_destroy",
             "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_tile_edge", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
+            "plugin_shard_tiles", "plugin_tile_edge", "plugin_work_item", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
             "kde_workspace_bytes", "kde_eval", "kde_prepare",
             "kde_eval_prepared", "plugin_last_error", "plugin_version")
 
@@ -359,6 +360,14 @@ def plugin_num_tiles(n: int) -> int:
 
 def plugin_tile_edge(n: int) -> int:
     return lib().plugin_tile_edge(n)
+
+
+def plugin_work_item(n: int, item: int) -> tuple[tuple[int, int], tuple[int, int], int]:
+    """The pairs of work item `item`: (row range, column range, weight) in sorted indices."""
+    out = (ctypes.c_int64 * 5)()
+    if lib().plugin_work_item(n, item, out) != 0:
+        raise IndexError(f"work item {item} out of range for n={n}")
+    return (out[0], out[1]), (out[2], out[3]), out[4]
 
 
 def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:

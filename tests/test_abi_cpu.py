@@ -67,6 +67,39 @@ def test_tiles_cover_triangle(L, n):
     assert L.plugin_shard_tiles(n, 3, 2) == (0, 0)    # invalid rank -> empty range
 
 
+@pytest.mark.parametrize("n", [1, 2, 2048, 2049, 5000, 16384, 50000, 131072, 1 << 20])
+def test_work_items_partition_the_triangle(n):
+    # every tile's columns are covered exactly once by its items (whole, or 4 quarters), rows
+    # and weights are the tile's; the items cover exactly the upper block triangle
+    from paper_1505_02100_b200 import plugin as P
+    T, items = P.plugin_tile_edge(n), P.plugin_num_tiles(n)
+    nb = -(-n // T)
+    cover = {}
+    step = max(1, items // 4000)  # large n: a deterministic sample of items plus all tail items
+    idx = sorted(set(range(0, items, step)) | set(range(max(0, items - 8 * 444 * 4), items)))
+    for it in idx:
+        (r0, r1), (c0, c1), w = P.plugin_work_item(n, it)
+        bi, bj = r0 // T, (c0 // T) if c1 > c0 else None
+        assert r0 == bi * T and r1 == min(n, r0 + T) and 0 <= r0 < r1 <= n
+        if bj is None:
+            continue                       # a quarter past the sample's end: no pairs
+        assert bj >= bi and w == (1 if bi == bj else 2) and c1 <= min(n, bj * T + T)
+        cover.setdefault((bi, bj), []).append((c0, c1))
+    if step == 1:
+        assert len(cover) == nb * (nb + 1) // 2
+    for (bi, bj), spans in cover.items():
+        spans.sort()
+        full = [(bj * T, min(n, bj * T + T))]
+        if len(spans) == 1 or spans[0][1] - spans[0][0] == full[0][1] - full[0][0]:
+            assert spans == full or len(spans) == 1
+        else:                              # quarters: contiguous, disjoint, ending at the block's end
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0
+            assert spans[0][0] == full[0][0] and spans[-1][1] == full[0][1]
+    with pytest.raises(IndexError):
+        P.plugin_work_item(n, items)
+
+
 def test_kde_workspace_sizing(L):
     # the psi workspace (sorted copy of X) plus per-(block, segment) fp64 partials, bounded by
     # (8 * 148 target CTAs + one per point block) x 1024 points x 8 bytes

@@ -248,9 +248,6 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
     res.status, res.n, res.g1, res.g2 = 0, n, g1, g4
     dres = torch.frombuffer(bytearray(bytes(res)), dtype=torch.uint8).cuda()
     zs = np.sort(oracle_mod.widen(x))
-    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
-    nb = -(-n // T)
-    assert nb * (nb + 1) // 2 == ntiles
     world = 1024
     phi0 = 1 / math.sqrt(2 * math.pi)
     for r, g in ((6, g1), (4, g4)):
@@ -258,20 +255,12 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
             part = P.new_partial()
             P.psi_r_shard(n, r, rank, world, dres, part, ws)
             got = from_limbs(part.cpu().tolist()) / 2.0 ** 64 * phi0
-            tb, te = P.plugin_shard_tiles(n, rank, world)
-            runs = {}                       # tile row bi -> (first bj, last bj) of this shard
-            for t in range(tb, te):
-                bi, bj = _tile_coords(t, nb)
-                lo, hi = runs.get(bi, (bj, bj))
-                runs[bi] = (min(lo, bj), max(hi, bj))
+            ib, ie = P.plugin_shard_tiles(n, rank, world)
             ref = 0.0
-            for bi, (lo, hi) in runs.items():
-                rows = (bi * T, min(n, bi * T + T))
-                if lo == bi:                # diagonal tile: full square, weight 1
-                    ref += oracle_mod.psi_block_sum(zs, g, r, *rows, bi * T, min(n, bi * T + T))
-                    lo += 1
-                if lo <= hi:                # off-diagonal tiles: weight 2
-                    ref += 2.0 * oracle_mod.psi_block_sum(zs, g, r, *rows, lo * T, min(n, hi * T + T))
+            for it in range(ib, ie):        # each work item: a tile or a tail-tile quarter
+                rows, cols, w = P.plugin_work_item(n, it)
+                if cols[1] > cols[0]:
+                    ref += w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols)
             assert rel(got, ref) < TOL, (k, r, rank, got, ref, rel(got, ref))
 
 
@@ -570,16 +559,13 @@ def test_plugin_h_on_a_second_device(P):
     assert _same(a, b)
 
 
-def _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb):
-    bi, bj = _tile_coords(t, nb)
-    rows = (bi * T, min(n, bi * T + T))
-    cols = (bj * T, min(n, bj * T + T))
-    w = 1.0 if bi == bj else 2.0
-    return w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols)
+def _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t):
+    rows, cols, w = P.plugin_work_item(n, t)
+    return w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols) if cols[1] > cols[0] else 0.0
 
 
 def _one_tile(P, n, r, t, ntiles, dres, ws):
-    """The exact fixed-point sum of tile t alone (psi_r_shard with one tile per 'rank')."""
+    """The exact fixed-point sum of work item t alone (psi_r_shard with one item per 'rank')."""
     from paper_1505_02100_b200.distributed import from_limbs
     part = P.new_partial()
     P.psi_r_shard(n, r, t, ntiles, dres, part, ws)
@@ -617,11 +603,11 @@ def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
         dres = _bandwidth_record(P, n, g, g)
         for t in picks:
             got = _one_tile(P, n, r, t, ntiles, dres, ws)
-            ref = _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb)
+            ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
             assert math.isfinite(got)
             # relative 1e-5; terms below the fp32 range (e^(-u^2/2) < 2^-126: the far tiles) are
             # +0 on the GPU, so an absolute T^2 2^-100 is allowed on top
-            assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (n, r, t, _tile_coords(t, nb), got, ref)
+            assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (n, r, t, P.plugin_work_item(n, t), got, ref)
 
 
 @pytest.mark.parametrize("r", [8, 12])
@@ -641,5 +627,5 @@ def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
     dres = _bandwidth_record(P, n, g, g)
     for t in (0, 5, nb + 3, ntiles // 2, ntiles // 2 + 1, ntiles - 3, ntiles - 1):
         got = _one_tile(P, n, r, t, ntiles, dres, ws)
-        ref = _tile_sum_oracle(oracle_mod, zs, g, r, n, T, t, nb)
-        assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, _tile_coords(t, nb), got, ref)
+        ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
+        assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, P.plugin_work_item(n, t), got, ref)
