@@ -36,14 +36,14 @@ __device__ __forceinline__ void dpi_bandwidth(plugin_dpi_result* out, int j, dou
   const int r = 2 * j + 2;
   const double num = -2.0 * k_at_zero(r);
   if (!(num / psi_next > 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
-  const double g_z = pow(num / (kMu2 * psi_next * nd), 1.0 / (double)(r + 3));
+  const double g_z = plugin_bandwidth(num, psi_next, nd, r + 3);
   out->g_z[j - 1] = g_z;
   out->g[j - 1] = g_z * out->sigma;
 }
 
 __device__ __forceinline__ void dpi_h(plugin_dpi_result* out, double psi4_z, double nd) {
   if (!(psi4_z > 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
-  const double h_z = pow(kRK / (kMu2 * kMu2 * psi4_z * nd), 1.0 / 5.0);
+  const double h_z = plugin_h_z(psi4_z, nd);
   out->h_z = h_z;
   out->h = h_z * out->sigma;
 }

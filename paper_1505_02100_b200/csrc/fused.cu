@@ -14,6 +14,7 @@
 // Every tile sum, the fixed-point total and the scalar chain are computed by the same device
 // code as the multi-kernel path, so the result is bit-identical to it (tested).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "blocksort.cuh"
 #include "common.cuh"
@@ -29,7 +30,7 @@ namespace plg {
 #ifdef PLUGIN_FUSED_TIMING
 #define FT_MARK(k)                                                                   \
   do {                                                                               \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {                                       \
+    if ((blockIdx.x == 0 || (k) >= 7) && threadIdx.x == 0) { /* 7, 8: the last CTA */ \
       unsigned long long t;                                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                          \
       reinterpret_cast<unsigned long long*>(parts + 2 * kFusedMaxGrid)[k] = t;       \
@@ -113,6 +114,10 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
   // Steps IV/V and VI/VII
   cg::grid_group grid = cg::this_grid();
   const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
+  // pass 4's arrival counter (after the partials and the timing slots); zeroed by CTA 0 before
+  // the grid barrier of pass 6, incremented only after it
+  unsigned int* arrive = reinterpret_cast<unsigned int*>(parts + 2 * kFusedMaxGrid) + 32;
+  if (blockIdx.x == 0 && tid == 0) *arrive = 0u;
   for (int pass = 0; pass < 2; ++pass) {
     const bool ok = res.status == PLUGIN_OK;  // the same in every CTA
     if (ok) {
@@ -134,12 +139,24 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
       if (tid == 0) parts[pass * gridDim.x + blockIdx.x] = acc;
     }
     FT_MARK(3 + 3 * pass);
-    grid.sync();
+    if (pass == 0) {
+      grid.sync();  // every CTA needs g2 from the whole Step IV sum
+    } else {
+      // Step VI: only the last CTA to arrive reduces and finalises (threadfence pattern): no
+      // second grid barrier
+      __shared__ bool last;
+      if (tid == 0) {
+        __threadfence();
+        last = (atomicAdd(arrive, 1u) == gridDim.x - 1);
+      }
+      __syncthreads();
+      if (!last) return;
+      __threadfence();
+    }
     FT_MARK(4 + 3 * pass);
     if (ok) {
-      // every CTA adds all the partials: in parallel over the threads (independent L2 loads),
-      // then a 128-bit shuffle / shared-memory reduction -- integer addition, so any order
-      // gives the same total
+      // the partials: in parallel over the threads (independent L2 loads), then a 128-bit
+      // shuffle / shared-memory reduction -- integer addition, so any order gives the same total
       Fx128 tot = {0ull, 0ll};
       for (unsigned int b = tid; b < gridDim.x; b += kPsiThreads) fx_add(tot, ldcg_fx(parts + pass * gridDim.x + b));
       for (int o = 16; o; o >>= 1) {
@@ -159,7 +176,8 @@ plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, p
     }
     FT_MARK(5 + 3 * pass);
   }
-  if (blockIdx.x == 0 && tid == 0) *out = res;
+  // the last CTA of pass 4 (every CTA holds the same record up to here)
+  if (tid == 0) *out = res;
 }
 
 // Many small samples in one launch (plugin_h_batch): CTA b runs the whole algorithm for sample
@@ -272,6 +290,10 @@ cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out
   const int sms = dev_cached(sm_cache, device_sms);
   int grid = (int)(tiles < max_grid ? tiles : max_grid);
   if (grid > sms) grid = sms;
+  if (const char* e = getenv("PLUGIN_FUSED_GRID")) {  // A/B only: fewer CTAs (cheaper barriers)
+    const int g = atoi(e);
+    if (g >= 1 && g < grid) grid = g;
+  }
   size_t smem = sizeof(float) * ((size_t)nsx + kBlockSortN);  // sample + sort scratch
   void* args[] = {(void*)&x, (void*)&n, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
   return cudaLaunchCooperativeKernel((const void*)plugin_fused_kernel<0>, dim3(grid), dim3(kPsiThreads), args, smem,

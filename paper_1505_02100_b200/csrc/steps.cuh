@@ -15,6 +15,41 @@ __device__ __forceinline__ double ipow(double b, int k) {
   return r;
 }
 
+// w^(-1/k) for finite w > 0, 1 <= k <= 15: a float seed 2^(-log2(w) / k) (MUFU lg2 / ex2 on the
+// mantissa, the exponent split off so the seed cannot leave float range), then three Newton steps
+// z <- z + z (1 - w z^k) / k in fp64 -- no division; quadratic convergence from the ~1e-6 seed
+// to the fp64 fixed point (within a few ulp of the exact root).  A compact rolled loop: the
+// library pow costs ~1 us of latency per call in the single-launch kernel (profiles/r02r_*).
+__device__ __forceinline__ double inv_root(double w, int k) {
+  int e;
+  const double m = frexp(w, &e);  // w = m 2^e, m in [0.5, 1)
+  const double t = -((double)__log2f((float)m) + (double)e) / (double)k;
+  const double ti = floor(t);
+  double z = ldexp((double)exp2f((float)(t - ti)), (int)ti);
+  const double rk = 1.0 / (double)k;
+#pragma unroll 1
+  for (int it = 0; it < 3; ++it) {
+    double zk = 1.0, b = z;  // z^k by squaring
+#pragma unroll 1
+    for (int q = k; q; q >>= 1) {
+      if (q & 1) zk *= b;
+      b *= b;
+    }
+    z = fma(z * fma(-w, zk, 1.0), rk, z);
+  }
+  return z;
+}
+
+// the bandwidths of Algorithm 1 and of the l-stage family (Steps III and V):
+// g = (num / (mu2 Psi n))^(1/k) = (mu2 Psi n / num)^(-1/k), num = -2 K^(r)(0), k = r + 3
+__device__ __forceinline__ double plugin_bandwidth(double num, double psi, double nd, int k) {
+  return inv_root(kMu2 * psi * nd / num, k);
+}
+// Step VII: h_z = (R(K) / (mu2^2 Psi4 n))^(1/5)
+__device__ __forceinline__ double plugin_h_z(double psi4_z, double nd) {
+  return inv_root(kMu2 * kMu2 * psi4_z * nd / kRK, 5);
+}
+
 // Step I, one block's share: V is shift invariant, so it is evaluated on
 // d_i = X_i - X_0 (exact in fp64) with the printed one-pass form; this block (index b of
 // nblocks, 256 threads) sums d and d^2 over i = b*256 + tid + k*nblocks*256.  Thread 0
@@ -75,7 +110,7 @@ __device__ __forceinline__ void step1_epilogue(double a, double q, int64_t n, do
   const double psi8_z = 105.0 / (32.0 * sqrt(kPi));
   out->psi8_ns = psi8_z / ipow(sigma, 9);
   // Step III
-  const double g1_z = pow(-2.0 * kK6at0 / (kMu2 * psi8_z * nd), 1.0 / 9.0);
+  const double g1_z = plugin_bandwidth(-2.0 * kK6at0, psi8_z, nd, 9);
   out->g1_z = g1_z;
   out->g1 = g1_z * sigma;
 }
@@ -99,7 +134,7 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
     out->psi6 = psi6_z / ipow(sigma, 7);
     if (!(psi6_z < 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
     // Step V
-    const double g2_z = pow(-2.0 * kK4at0 / (kMu2 * psi6_z * nd), 1.0 / 7.0);
+    const double g2_z = plugin_bandwidth(-2.0 * kK4at0, psi6_z, nd, 7);
     out->g2_z = g2_z;
     out->g2 = g2_z * sigma;
   } else {
@@ -111,7 +146,7 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
     out->psi4 = psi4_z / ipow(sigma, 5);
     if (!(psi4_z > 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
     // Step VII and Eq. 4
-    const double h_z = pow(kRK / (kMu2 * kMu2 * psi4_z * nd), 1.0 / 5.0);
+    const double h_z = plugin_h_z(psi4_z, nd);
     out->h_z = h_z;
     out->h = h_z * sigma;
   }

@@ -21,9 +21,11 @@ def main():
     for n in [int(a) for a in sys.argv[1:]] or [128, 512, 1024, 2048]:
         x = torch.from_numpy(inputs.normal(n, 7)).cuda()
         ws = P.workspace(n, x.device)
-        # the timing slots follow the 2 * 1024 Fx128 partials of the fused region; find that region
-        # as the last 32 KB + 256 B of the workspace layout (the result slot precedes it)
-        off = ws.numel() - (2 * 1024 * 16 + 256)
+        # the timing slots follow the 2 * 1024 Fx128 partials of the fused region (abi.cu layout:
+        # ctrl | step1 partials | xs | tmp | radix histograms | result | fused | group arrays)
+        def up(v):
+            return (v + 255) // 256 * 256
+        off = up(512) + up(16 * 592) + 2 * up(4 * max(n, 1)) + up(4 * 256 * max(1, -(-n // 2048))) + up(P.RESULT_BYTES)
         acc = {k: [] for k in NAMES}
         for it in range(30):
             P.plugin_h(x, ws=ws)
