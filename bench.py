@@ -33,6 +33,26 @@ sys.path.insert(0, ROOT)
 METRIC = "pairwise K4/K6 evaluations/sec (GPairs/s) and end-to-end h time vs FMA/SFU roofline, 1-8 GPUs"
 UNIT = "GPairs/s"
 MUFU_EX2_PER_CLK_PER_SM = 16      # measured: tools/probe/mufu_probe.cu (profiles/r01_mufu_probe.jsonl)
+FMA_LANE_OPS_PER_CLK_PER_SM = 128  # FP32 lane-ops (packed FFMA2 = 2), measured 124-128 (r01_mufu_probe.jsonl)
+EX2_FMA_LANE_OPS = 8               # simd.cuh ex2_fma2: an FMA-pipe 2^x costs 8 FP32 lane-ops per lane
+
+
+def dual_pipe_bound(fp32_ops: float) -> float:
+    """Pairs (terms) per clock per SM when a fraction phi of the exps runs on the FMA pipe
+    (ex2_fma2) and the rest on MUFU.EX2, at the best phi: min(16 / (1 - phi), 128 / (k + 8 phi)) is
+    largest where both pipes saturate, phi = (128 - 16 k) / (128 + 16 * 8).  k = FP32 lane-ops per
+    pair besides the exp: 7 (psi6), 6 (psi4), 3 (KDE, centred)."""
+    phi = (FMA_LANE_OPS_PER_CLK_PER_SM - MUFU_EX2_PER_CLK_PER_SM * fp32_ops) / (
+        FMA_LANE_OPS_PER_CLK_PER_SM + MUFU_EX2_PER_CLK_PER_SM * EX2_FMA_LANE_OPS)
+    phi = max(0.0, phi)
+    return min(MUFU_EX2_PER_CLK_PER_SM / (1.0 - phi), FMA_LANE_OPS_PER_CLK_PER_SM / (fp32_ops + EX2_FMA_LANE_OPS * phi))
+
+
+# Q32.32 pass (q32.cu): the ALU pipe binds (ncu on an all-in-range pass, profiles/r02_prof_q32_summary.txt:
+# ALU 64% of peak, FMA/IMAD 26%, XU 0%); 169 ALU-pipe thread-instructions per in-range pair
+# (sm__inst_executed_pipe_alu x 32 / pairs) at 64 ALU lanes/clk/SM (16 per SMSP, rt 2)
+Q32_ALU_INST_PER_PAIR = 169.0
+ALU_LANES_PER_CLK_PER_SM = 64
 # kernels of one step, n > 32768 (group.cu: from kGroupMinN = 32768 the distinct-value count and
 # compaction run after Step I, and each pass launches the fp32 tile pass and the grouped exact
 # pass, one of which returns at once)
@@ -386,7 +406,13 @@ def run_ours(a):
                          "traffic": _traffic(n), "kernel": "psi_kernel (r=6 and r=4 pass average)",
                          "peak_basis": f"{MUFU_EX2_PER_CLK_PER_SM} MUFU.EX2/clk/SM x {sms} SMs x measured median "
                                        f"SM clock {f_meas:.0f} MHz (1 ex2 per pair)",
-                         "frac_at_1965MHz": achieved / (MUFU_EX2_PER_CLK_PER_SM * sms * 1.965)},
+                         "frac_at_1965MHz": achieved / (MUFU_EX2_PER_CLK_PER_SM * sms * 1.965),
+                         # the same against the dual-pipe bound (some exps on the FMA pipe, both pipes
+                         # saturated): 17.07 (psi6) / 18.29 (psi4) pairs/clk/SM; the passes evaluate all
+                         # exps on MUFU, so this is the headroom a hybrid exp could take
+                         "frac_dual_pipe": achieved / (2.0 / (1.0 / dual_pipe_bound(7) + 1.0 / dual_pipe_bound(6))
+                                                       * sms * f_meas * 1e6 / 1e9),
+                         "dual_pipe_pairs_per_clk_per_sm": {"psi6": dual_pipe_bound(7), "psi4": dual_pipe_bound(6)}},
             "passes": {"psi6_gpairs_s": per_launch_pairs * world / (k6_ms / a.steps / 1e3) / 1e9,
                        "psi4_gpairs_s": per_launch_pairs * world / (k4_ms / a.steps / 1e3) / 1e9,
                        "psi6_ms": k6_ms / a.steps, "psi4_ms": k4_ms / a.steps},
@@ -512,7 +538,10 @@ def run_kde(a):
                                         + ("MUFU.EX2-bound, 1 ex2 per visited term" if mufu_only else
                                            "12/16 of the exps on MUFU.EX2 (the binding pipe), 4/16 on the FMA "
                                            "pipe, centred terms") + ")"),
-                         "variant": "mufu_only" if mufu_only else "hybrid"},
+                         "variant": "mufu_only" if mufu_only else "hybrid",
+                         # the LP optimum of the centred 3-op term (5/16 FMA-pipe exps, both pipes saturated)
+                         "frac_dual_pipe": achieved / (dual_pipe_bound(3) * sms * f_meas * 1e6 / 1e9),
+                         "dual_pipe_terms_per_clk_per_sm": dual_pipe_bound(3)},
             "e2e": {"value": n * m / statistics.median(ts) / 1e9, "unit": "GTerms/s",
                     "h2d_bytes_per_step": 4 * (n + m), "d2h_bytes_per_step": 8 * m,
                     "seconds_per_step": statistics.median(ts)},
@@ -583,6 +612,25 @@ def run_variant(a):
                             "kernel": "whole step (sort, Step I, the l pair passes)",
                             "peak_basis": f"{per_clk:.2f} pairs/clk/SM (passes r = {rs}: min(16 MUFU, 128/(4 + r/2) FMA))"
                                           f" x 148 SMs x {mhz:.0f} MHz"}
+    if a.workload == "q32":
+        # in-range pairs (|u| <= 7: the long path of q32_term; the others leave after two multiplies)
+        # counted on the host from the z-scores, at the ALU-pipe bound of an in-range pair
+        import numpy as np
+        z = np.sort((xh.astype(np.float64) - res["mean"]) / res["sigma"])
+        inrange = 0
+        for gz in (res["g1_z"], res["g2_z"]):
+            inrange += int((np.searchsorted(z, z + 7.0 * gz, side="right") - np.arange(z.size) - 1).sum())
+        mhz = clocks.get("sm_mhz") or 1965.0
+        per_clk = ALU_LANES_PER_CLK_PER_SM / Q32_ALU_INST_PER_PAIR
+        peak = per_clk * 148 * mhz * 1e6 / 1e9
+        achieved = inrange / (ms / 1e3) / 1e9
+        line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "GPairs/s (in-range)",
+                            "frac": achieved / peak, "traffic": None,
+                            "kernel": "whole step (sort, Step I, encode, the two Q32.32 passes)",
+                            "in_range_pairs": inrange, "pairs": pairs,
+                            "peak_basis": f"{per_clk:.3f} in-range pairs/clk/SM = {ALU_LANES_PER_CLK_PER_SM} ALU "
+                                          f"lanes/clk/SM / {Q32_ALU_INST_PER_PAIR:.0f} ALU-pipe instructions per "
+                                          f"in-range pair (ncu) x 148 SMs x {mhz:.0f} MHz"}
     print(json.dumps(line), flush=True)
     return 0
 
