@@ -194,6 +194,10 @@ __device__ __forceinline__ void pair2_fma(u64 xj, u64 xi, u64 s2, u64 ph, u64& a
 #ifndef PSI_HYB4
 #define PSI_HYB4 0
 #endif
+// the same for r = 6: 1 pair in 16 on the FMA pipe (min(16 / (15/16), 128 / (7 + 8/16)) = 17.07)
+#ifndef PSI_HYB6
+#define PSI_HYB6 0
+#endif
 
 __device__ __forceinline__ Fx128 fx_from_double(double x) {
   Fx128 r;
@@ -271,7 +275,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
           continue;
         }
         pair2<ORDER, false, CEN>(j01, xi[k], s2[k], ph[k], acc[k]);
-        if (PSI_HYB4 && ORDER == 4 && R == 8 && (k == (q & 7) || k == ((q + 4) & 7)))
+        if ((PSI_HYB4 && ORDER == 4 && R == 8 && (k == (q & 7) || k == ((q + 4) & 7))) ||
+            (PSI_HYB6 && ORDER == 6 && R == 8 && k == (q & 7)))
           pair2_fma<ORDER, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
         else
           pair2<ORDER, false, CEN>(j23, xi[k], s2[k], ph[k], acc[k]);
