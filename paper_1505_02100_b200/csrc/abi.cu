@@ -150,7 +150,10 @@ void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t*
 
 const char* plugin_last_error(void) { return g_err; }
 
-const char* plugin_version(void) { return "libplugin 0.1 sm_100a (psi: f32x2 + MUFU.EX2, dithered; fx128 accumulation)"; }
+const char* plugin_version(void) {
+  return "libplugin 0.2 sm_100a (psi: f32x2 + MUFU.EX2, exact-staging centre, antithetic dither; "
+         "grouped fp64 pass for tied samples; fx128 accumulation)";
+}
 
 plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out, void* d_ws, size_t ws_bytes, void* stream) {
   return plugin_h_ex(d_x, n, d_out, 0u, d_ws, ws_bytes, stream);
