@@ -127,9 +127,9 @@ plugin_status plugin_graph_create(const float* d_x, int64_t n, plugin_result* d_
 plugin_status plugin_graph_launch(plugin_graph* graph, void* stream);
 void plugin_graph_destroy(plugin_graph* graph);
 
-/* Same as plugin_h (device result kept in the workspace), then synchronises `stream`,
- * copies the result to *h_out and returns its data status (PLUGIN_OK or one of
- * E_NONFINITE/E_DEGENERATE/E_DOMAIN). */
+/* Same as plugin_h -- Algorithm 1, X -> h (Eq. 3-4) -- with the device result kept in
+ * the workspace, then synchronises `stream`, copies the result to *h_out and returns its data
+ * status (PLUGIN_OK or one of E_NONFINITE/E_DEGENERATE/E_DOMAIN). */
 plugin_status plugin_h_sync(const float* d_x, int64_t n, plugin_result* h_out,
                             void* d_ws, size_t ws_bytes, void* stream);
 
@@ -153,8 +153,9 @@ plugin_status psi_r(const float* d_x, int64_t n, double g, int r, double* d_psi,
 
 /* ---- multi-GPU building blocks (one process per GPU; the caller allreduces) ---- */
 
-/* Step I..III on this rank's full copy of X: fills mean, var, sigma, psi8_ns, g1(_z),
- * status in d_out and prepares the workspace (sorted X) for the psi shards. */
+/* Steps I-III (V, sigma, Psi8^NS, g1) on this rank's full copy of X: fills mean, var,
+ * sigma, psi8_ns, g1(_z), status in d_out and prepares the workspace (the sorted X, and the
+ * distinct-value arrays of a heavily tied sample) for the psi shards.  Asynchronous. */
 plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
                            void* d_ws, size_t ws_bytes, void* stream);
 
@@ -169,8 +170,24 @@ plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
 plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_result* d_out,
                           plugin_fx128* d_partial, void* d_ws, size_t ws_bytes, void* stream);
 
-/* Finalize a pass from the all-reduced fixed-point total: psi6 and g2 (r=6), or
- * psi4 and h (r=4), into d_out (data status E_DOMAIN if the sign check fails). */
+/* The same share at a bandwidth of the caller's choosing (SURVEY §8(b)'s psi_r_shard(x, n, g, r,
+ * rank, world)): g (data units, finite > 0) from the host, any even r <= 12; the workspace must
+ * hold d_x's preparation (plugin_prepare or plugin_step1).  Summing the partials of all ranks and
+ * passing the total to plugin_psi_from_total gives psi_r(d_x, n, g, r) bit for bit. */
+plugin_status psi_r_shard_g(int64_t n, double g, int r, int rank, int world, plugin_fx128* d_partial,
+                            void* d_ws, size_t ws_bytes, void* stream);
+/* Sort d_x into the workspace and run Step I (non-finite check) and the distinct-value count:
+ * the preparation psi_r_shard_g needs.  Asynchronous. */
+plugin_status plugin_prepare(const float* d_x, int64_t n, void* d_ws, size_t ws_bytes, void* stream);
+/* Psi_r(g) = phi(0) S / (n^2 g^(r+1)) (Steps IV/VI) from the all-reduced fixed-point
+ * total S of psi_r_shard_g, into *d_psi (device double).  Asynchronous; one thread. */
+plugin_status plugin_psi_from_total(const plugin_fx128* d_total, int64_t n, double g, int r, double* d_psi,
+                                    void* stream);
+
+/* Finalize a pass from the all-reduced fixed-point total: Step IV's psi6 (Eq. 6) and
+ * Step V's g2 for r=6, or Step VI's psi4 (Eq. 7), Step VII's h_z
+ * and h = h_z sigma (Eq. 4) for r=4, into d_out (data status E_DOMAIN
+ * if psi6 >= 0 or psi4 <= 0).  Asynchronous; one thread. */
 plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 

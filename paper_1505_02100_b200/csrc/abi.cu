@@ -287,6 +287,57 @@ plugin_status psi_r_shard(int64_t n, int r, int rank, int world, const plugin_re
   return PLUGIN_OK;
 }
 
+plugin_status plugin_prepare(const float* d_x, int64_t n, void* d_ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_x) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(w.ctrl, 0, sizeof(Ctrl), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset ctrl");
+  if ((e = launch_sort(d_x, n, w.xs, w.tmp, w.hist, w.L.sort_blocks, s)) != cudaSuccess) return cuda_fail(e, "sort");
+  plugin_result* scratch = reinterpret_cast<plugin_result*>(static_cast<char*>(d_ws) + w.L.result);
+  if ((e = launch_step1(w.xs, n, w.ctrl, w.step1, scratch, s)) != cudaSuccess) return cuda_fail(e, "step1");
+  if ((e = launch_group_build(w.xs, n, w.ctrl, w.grp_heads, w.grp_v, w.grp_s, scratch, s)) != cudaSuccess)
+    return cuda_fail(e, "group");
+  return PLUGIN_OK;
+}
+
+plugin_status psi_r_shard_g(int64_t n, double g, int r, int rank, int world, plugin_fx128* d_partial, void* d_ws,
+                            size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!d_partial) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  if (r < 0 || r > 12 || (r & 1)) return fail(PLUGIN_E_INVALID, "r must be even, 0..12%s (r=%lld)", "", r);
+  if (!(std::isfinite(g) && g > 0.0)) return fail(PLUGIN_E_INVALID, "g must be finite and > 0%s");
+  if (world < 1 || rank < 0 || rank >= world) return fail(PLUGIN_E_INVALID, "bad rank/world%s");
+  WS w;
+  if ((st = get_ws(d_ws, ws_bytes, n, w)) != PLUGIN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = pass(w, n, r, 0, g, nullptr, nullptr, 1, rank, world, s, PsiFin());
+  if (e != cudaSuccess) return cuda_fail(e, "psi shard");
+  if ((e = launch_finalize(3, w.ctrl, 1, nullptr, nullptr, n, 0.0, r, nullptr, d_partial, s)) != cudaSuccess)
+    return cuda_fail(e, "export partial");
+  return PLUGIN_OK;
+}
+
+plugin_status plugin_psi_from_total(const plugin_fx128* d_total, int64_t n, double g, int r, double* d_psi,
+                                    void* stream) {
+  g_err[0] = 0;
+  if (!d_total || !d_psi) return fail(PLUGIN_E_INVALID, "null pointer argument%s");
+  plugin_status st = check_n(n, 1);
+  if (st != PLUGIN_OK) return st;
+  if (r < 0 || r > 12 || (r & 1)) return fail(PLUGIN_E_INVALID, "r must be even, 0..12%s (r=%lld)", "", r);
+  if (!(std::isfinite(g) && g > 0.0)) return fail(PLUGIN_E_INVALID, "g must be finite and > 0%s");
+  cudaError_t e = launch_finalize(2, nullptr, 0, d_total, nullptr, n, g, r, d_psi, nullptr,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "finalize");
+  return PLUGIN_OK;
+}
+
 static plugin_status after(int what, const plugin_fx128* d_total, plugin_result* d_out, void* stream) {
   g_err[0] = 0;
   if (!d_total || !d_out) return fail(PLUGIN_E_INVALID, "null pointer argument%s");

@@ -88,6 +88,9 @@ def lib():
             "plugin_num_tiles": (i64, [i64]),
             "plugin_tile_edge": (i64, [i64]),
             "plugin_work_item": (i32, [i64, i64, ctypes.POINTER(i64)]),
+            "psi_r_shard_g": (i32, [i64, d, i32, i32, i32, P, P, sz, P]),
+            "plugin_prepare": (i32, [P, i64, P, sz, P]),
+            "plugin_psi_from_total": (i32, [P, i64, d, i32, P, P]),
             "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
             "plugin_sort": (i32, [P, i64, P, P, sz, P]),
@@ -119,7 +122,8 @@ EXPORTED = ("plugin_workspace_bytes", "plugin_host_workspace_bytes", "plugin_h",
             "plugin_graph_create", "plugin_graph_launch", "plugin_graph_destroy",
             "plugin_h_sync", "plugin_h_host",
             "psi_r", "plugin_step1", "psi_r_shard", "plugin_after_psi6", "plugin_after_psi4", "plugin_num_tiles",
-            "plugin_shard_tiles", "plugin_tile_edge", "plugin_work_item", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
+            "plugin_shard_tiles", "plugin_tile_edge", "plugin_work_item", "psi_r_shard_g", "plugin_prepare",
+            "plugin_psi_from_total", "plugin_dpi", "plugin_sort", "plugin_q32_workspace_bytes", "psi_r_q32", "plugin_h_q32",
             "kde_workspace_bytes", "kde_eval", "kde_prepare",
             "kde_eval_prepared", "plugin_last_error", "plugin_version")
 
@@ -340,6 +344,33 @@ def psi_r_shard(n: int, r: int, rank: int, world: int, out: torch.Tensor, partia
         _check(lib().psi_r_shard(n, r, rank, world, out.data_ptr(), partial.data_ptr(), ws.data_ptr(), ws.numel(),
                                  on.handle))
     return partial
+
+
+def plugin_prepare(x: torch.Tensor, ws: torch.Tensor, stream=None) -> torch.Tensor:
+    """Sort X into the workspace, Step I and the distinct-value count (for psi_r_shard_g)."""
+    with _On(_dev(x), stream) as on:
+        x = _x(x)
+        on.uses(x)
+        _check(lib().plugin_prepare(x.data_ptr(), x.numel(), ws.data_ptr(), ws.numel(), on.handle))
+    return ws
+
+
+def psi_r_shard_g(n: int, g: float, r: int, rank: int, world: int, partial: torch.Tensor, ws: torch.Tensor,
+                  stream=None) -> torch.Tensor:
+    """This rank's share of Psi_r at a host bandwidth g, as 4 fixed-point limbs (int64[4])."""
+    with _On(ws.device, stream) as on:
+        _check(lib().psi_r_shard_g(int(n), float(g), int(r), int(rank), int(world), partial.data_ptr(),
+                                   ws.data_ptr(), ws.numel(), on.handle))
+    return partial
+
+
+def plugin_psi_from_total(total: torch.Tensor, n: int, g: float, r: int, out: torch.Tensor | None = None,
+                          stream=None) -> torch.Tensor:
+    """Psi_r(g) from the all-reduced limbs of psi_r_shard_g (device float64[1])."""
+    with _On(total.device, stream) as on:
+        out = torch.empty(1, dtype=torch.float64, device=total.device) if out is None else out
+        _check(lib().plugin_psi_from_total(total.data_ptr(), int(n), float(g), int(r), out.data_ptr(), on.handle))
+    return out
 
 
 def plugin_after_psi6(total: torch.Tensor, out: torch.Tensor, stream=None):

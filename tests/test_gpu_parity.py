@@ -629,3 +629,25 @@ def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
         got = _one_tile(P, n, r, t, ntiles, dres, ws)
         ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
         assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, P.plugin_work_item(n, t), got, ref)
+
+
+@pytest.mark.parametrize("case", ["cfg2", "ties_grouped", "small"])
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_psi_r_shard_g_sums_to_psi_r_bit_exact(P, case, world):
+    # the explicit-bandwidth shard of SURVEY §8(b): every rank's partial at a host g, limbs
+    # summed (what the NCCL allreduce does), finalised -> psi_r's bits, r = 6, 4 and 8
+    x = {"cfg2": lambda: inputs.config_data(2), "ties_grouped": lambda: inputs.ties(40000, 31),
+         "small": lambda: inputs.normal(777, 32)}[case]()
+    xt = torch.from_numpy(x).cuda()
+    n = x.size
+    ws = P.workspace(n)
+    P.plugin_prepare(xt, ws)
+    for r, g in ((6, 0.4), (4, 0.3), (8, 0.55)):
+        tot = torch.zeros(4, dtype=torch.int64, device="cuda")
+        for rank in range(world):
+            part = P.new_partial()
+            P.psi_r_shard_g(n, g, r, rank, world, part, ws)
+            tot += part
+        got = P.plugin_psi_from_total(tot, n, g, r).item()
+        ref = P.psi_r(xt, g, r).item()
+        assert got == ref, (case, world, r, got, ref)
