@@ -146,3 +146,33 @@ def test_grouped_permutation_and_graph(P):
     for k in ("psi6", "psi4", "h"):
         assert a[k] == b[k] == c[k]
     assert not math.isnan(a["h"])
+
+
+@pytest.mark.parametrize("n", [32767, 32768])
+def test_group_min_n_boundary(P, oracle_mod, n):
+    # kGroupMinN = 32768: a heavily tied sample one below takes the fp32 pass (1e-5), at it the
+    # grouped exact pass (fp64)
+    x = inputs.ties(n, 41)
+    r = P.plugin_h_sync(torch.from_numpy(x).cuda())
+    o = oracle_mod.plugin(x)
+    grouped = bool(r["path"] & P.PLUGIN_PATH_GROUPED)
+    assert grouped == (n >= 32768)
+    tol = TOL_FP64 if grouped else 1e-5
+    for key in ("psi6_z", "psi4_z", "h"):
+        assert rel(r[key], o[key]) < tol, (n, key, r[key], o[key])
+
+
+def test_grouped_flags_and_statuses(P):
+    x = TIED["integers"]()
+    xt = torch.from_numpy(x).cuda()
+    a = P.read_result(P.plugin_h(xt))
+    b = P.read_result(P.plugin_h(xt, flags=P.PLUGIN_SKIP_UNDERFLOW))   # the grouped pass skips exactly too
+    assert a["path"] & P.PLUGIN_PATH_GROUPED and all(a[k] == b[k] for k in a)
+    # a non-finite value or zero variance: the data status wins, no grouped pass
+    bad = x.copy()
+    bad[123] = np.nan
+    r = P.plugin_h_sync(torch.from_numpy(bad).cuda())
+    assert r["status"] == P.PLUGIN_E_NONFINITE and not (r["path"] & P.PLUGIN_PATH_GROUPED) and math.isnan(r["h"])
+    const = np.full(40000, 2.5, np.float32)
+    r = P.plugin_h_sync(torch.from_numpy(const).cuda())
+    assert r["status"] == P.PLUGIN_E_DEGENERATE and math.isnan(r["h"])
