@@ -49,7 +49,7 @@ Layout layout(int64_t n) {
   L.grp_v = off;
   off = align_up(off + sizeof(float) * (nn / 4 + 1), 256);
   L.grp_s = off;
-  off = align_up(off + sizeof(int) * (nn / 4 + 2), 256);
+  off = align_up(off + sizeof(long long) * (nn / 4 + 2), 256);
   L.total = off;
   return L;
 }
@@ -63,7 +63,7 @@ struct WS {
   unsigned int* hist;
   unsigned int* grp_heads;
   float* grp_v;
-  int* grp_s;
+  long long* grp_s;
 };
 
 static plugin_status get_ws(void* d_ws, size_t ws_bytes, int64_t n, WS& w) {
@@ -80,7 +80,7 @@ static plugin_status get_ws(void* d_ws, size_t ws_bytes, int64_t n, WS& w) {
   w.hist = reinterpret_cast<unsigned int*>(b + w.L.hist);
   w.grp_heads = reinterpret_cast<unsigned int*>(b + w.L.grp_heads);
   w.grp_v = reinterpret_cast<float*>(b + w.L.grp_v);
-  w.grp_s = reinterpret_cast<int*>(b + w.L.grp_s);
+  w.grp_s = reinterpret_cast<long long*>(b + w.L.grp_s);
   return PLUGIN_OK;
 }
 

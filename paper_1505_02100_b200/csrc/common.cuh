@@ -164,10 +164,10 @@ cudaError_t launch_dpi_init(const plugin_result* s1, int stages, plugin_dpi_resu
 cudaError_t launch_dpi_finalize(Ctrl* ctrl, int slot, int j, plugin_dpi_result* out, cudaStream_t s);
 // the grouped exact pass (group.cu): count the distinct values of the sorted copy and decide
 // (ctrl->grouped), compact them (gv values, gs run starts with gs[m] = n); then per pass
-cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned int* chunk_heads, float* gv, int* gs,
+cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned int* chunk_heads, float* gv, long long* gs,
                                const plugin_result* s1, cudaStream_t s);
 cudaError_t launch_group_psi(int64_t n, int r, double g_host, const double* g_dev, const int32_t* status_dev,
-                             Ctrl* ctrl, int slot, int rank, int world, const float* gv, const int* gs, cudaStream_t s,
+                             Ctrl* ctrl, int slot, int rank, int world, const float* gv, const long long* gs, cudaStream_t s,
                              PsiFin fin = PsiFin());
 // KDE of Eq. 1-2 at m points over the sorted sample xs (kde.cu); `extra` holds
 // kde_extra_bytes(n, m) bytes of workspace

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) group_count_kernel(const float* __restric
 // ---- compaction: gv[a] = v_a, gs[a] = first index of v_a in the sorted copy, gs[m] = n -----------
 __global__ void __launch_bounds__(256) group_write_kernel(const float* __restrict__ xs, int64_t n, const Ctrl* ctrl,
                                                           const unsigned int* __restrict__ chunk_base,
-                                                          float* __restrict__ gv, int* __restrict__ gs) {
+                                                          float* __restrict__ gv, long long* __restrict__ gs) {
   if (!ctrl->grouped) return;
   __shared__ unsigned int warp_sum[8];
   const int64_t c0 = (int64_t)blockIdx.x * kGroupChunk;
@@ -144,21 +144,21 @@ __global__ void __launch_bounds__(256) group_write_kernel(const float* __restric
     before += __popc(ballot & ((1u << lane) - 1u));
     if (head) {
       gv[before] = __ldg(xs + i);
-      gs[before] = (int)i;
+      gs[before] = (long long)i;
     }
     unsigned int step = 0;
     for (int w = 0; w < 8; ++w) step += warp_sum[w];
     __syncthreads();
     base += step;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) gs[ctrl->distinct] = (int)n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) gs[ctrl->distinct] = (long long)n;
 }
 
 // ---- the grouped pass ----------------------------------------------------------------------------
 template <int ORDER>
 __global__ void __launch_bounds__(kPsiThreads)
 group_psi_kernel(int64_t n, double g_host, const double* g_dev, const int32_t* status_dev, Ctrl* ctrl, int slot,
-                 int rank, int world, const float* __restrict__ gv, const int* __restrict__ gs, PsiFin fin) {
+                 int rank, int world, const float* __restrict__ gv, const long long* __restrict__ gs, PsiFin fin) {
   if (!ctrl->grouped) return;
   double g = g_host;
   if (g_dev) {
@@ -243,7 +243,7 @@ group_psi_kernel(int64_t n, double g_host, const double* g_dev, const int32_t* s
   finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
 }
 
-cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned int* chunk_heads, float* gv, int* gs,
+cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned int* chunk_heads, float* gv, long long* gs,
                                const plugin_result* s1, cudaStream_t s) {
   if (n < kGroupMinN) return cudaSuccess;  // never grouped: ctrl->grouped stays 0 (memset)
   const unsigned int chunks = (unsigned int)((n + kGroupChunk - 1) / kGroupChunk);
@@ -254,7 +254,7 @@ cudaError_t launch_group_build(const float* xs, int64_t n, Ctrl* ctrl, unsigned 
 
 template <int ORDER>
 static cudaError_t launch_g(int64_t n, double g, const double* g_dev, const int32_t* status_dev, Ctrl* ctrl, int slot,
-                            int rank, int world, const float* gv, const int* gs, cudaStream_t s, PsiFin fin) {
+                            int rank, int world, const float* gv, const long long* gs, cudaStream_t s, PsiFin fin) {
   static DevCache cap_cache;
   const int grid = dev_cached(cap_cache, [](int dev) {
     int occ = 0;
@@ -272,7 +272,7 @@ static cudaError_t launch_g(int64_t n, double g, const double* g_dev, const int3
 }
 
 cudaError_t launch_group_psi(int64_t n, int r, double g_host, const double* g_dev, const int32_t* status_dev,
-                             Ctrl* ctrl, int slot, int rank, int world, const float* gv, const int* gs, cudaStream_t s,
+                             Ctrl* ctrl, int slot, int rank, int world, const float* gv, const long long* gs, cudaStream_t s,
                              PsiFin fin) {
   if (n < kGroupMinN) return cudaSuccess;  // never grouped (ctrl->grouped stays 0)
   switch (r) {

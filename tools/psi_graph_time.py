@@ -69,6 +69,8 @@ def main():
             row[f"psi{r}_frac"] = round(pairs / (t * 1e-6) / 4.65312e12, 4)  # 16 ex2/clk/SM x 148 x 1965 MHz
         xo = P.new_result(x.device)
         row["plugin_h_us"] = round(graph_us(lambda: P.plugin_h(x, out=xo, ws=ws), reps=5), 2)
+        # the preparation alone: sort + Step I (+ the distinct count from n = 32768)
+        row["step1_sort_us"] = round(graph_us(lambda: P.plugin_step1(x, xo, ws), reps=10), 2)
         print(json.dumps(row), flush=True)
 
 
