@@ -651,3 +651,21 @@ def test_psi_r_shard_g_sums_to_psi_r_bit_exact(P, case, world):
         got = P.plugin_psi_from_total(tot, n, g, r).item()
         ref = P.psi_r(xt, g, r).item()
         assert got == ref, (case, world, r, got, ref)
+
+
+@pytest.mark.parametrize("n", [500, 1000, 2048])
+@pytest.mark.parametrize("kind", ["ties", "integers", "offset"])
+def test_small_n_discretised_single_launch_and_batch(P, oracle_mod, n, kind):
+    # n <= 2048 (the paper's sizes): the single launch (small tiles, difference first) and the
+    # batch kernel (T = 256 centred tiles, dither amplitude n/16) on discretised samples
+    x = {"ties": lambda: inputs.ties(n, 60 + n), "integers": lambda: np.round(inputs.normal(n, 61 + n, sd=4)).astype(np.float32),
+         "offset": lambda: inputs.offset(n, 62 + n)}[kind]()
+    o = oracle_mod.plugin(x)
+    xt = torch.from_numpy(x).cuda()
+    a = P.plugin_h_sync(xt)
+    off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+    b = P.read_results(P.plugin_h_batch(xt, off), 1)[0]
+    for r in (a, b):
+        assert r["status"] == 0
+        for key in ("psi6_z", "psi4_z", "h"):
+            assert rel(r[key], o[key]) < TOL, (kind, n, key, r[key], o[key])
