@@ -270,7 +270,8 @@ def run_skip(a):
     same = all(res[k] == ref[k] for k in ref if ref[k] == ref[k])
     ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.steps
     pairs = n * (n - 1) // 2
-    ev6, ev4 = psi_pairs_evaluated(xh, res["g1"]), psi_pairs_evaluated(xh, res["g2"])
+    ev6 = psi_pairs_evaluated(xh, res["g1"], P.plugin_tile_edge(n, 6))
+    ev4 = psi_pairs_evaluated(xh, res["g2"], P.plugin_tile_edge(n, 4))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
     peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9

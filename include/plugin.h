@@ -160,7 +160,7 @@ plugin_status plugin_step1(const float* d_x, int64_t n, plugin_result* d_out,
                            void* d_ws, size_t ws_bytes, void* stream);
 
 /* One rank's share of a psi pass (Steps IV/VI, Eq. 6/7):
- * the work items [w*rank/world, w*(rank+1)/world) of the pair triangle (w = plugin_num_tiles(n)),
+ * the work items [w*rank/world, w*(rank+1)/world) of the pair triangle (w = plugin_num_tiles(n, r)),
  * at the bandwidth of d_out (g1 for r=6, g2 for r=4 -- and g2 for the other even r <= 12 of
  * the plugin_dpi family, K^(r) = He_r phi), written as an unnormalised fixed-point
  * sum to *d_partial.  The items partition the pairs (sorted sample, upper block triangle,
@@ -191,20 +191,21 @@ plugin_status plugin_psi_from_total(const plugin_fx128* d_total, int64_t n, doub
 plugin_status plugin_after_psi6(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_out, void* stream);
 
-/* The pass's work items for n (a function of n only): T x T tiles of the sorted
- * sample's upper block triangle (T = plugin_tile_edge(n); diagonal tiles are full squares,
- * weight 1; off-diagonal weight 2), except that the last S + (tiles mod S) tiles (S = resident
- * CTAs of a B200) are split column-wise into 4 items each, so a pass ends on fine items.
- * plugin_num_tiles: the number of items; plugin_shard_tiles: the item range [begin, end) that
- * `rank` of `world` owns (what psi_r_shard processes, balanced to one item); plugin_work_item:
- * the pairs of one item, out5 = {row begin, row end, column begin, column end, weight} (sorted
- * indices), 0 on success, -1 if item is out of range.  Host-only; no CUDA call. */
-int64_t plugin_num_tiles(int64_t n);
-void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end);
-int plugin_work_item(int64_t n, int64_t item, int64_t* out5);
-/* The tile edge T of the pass for n (64 for n <= 2048, else 256 R with R the rows per
- * thread): the geometry of the items above (host-only; for tests and tools). */
-int64_t plugin_tile_edge(int64_t n);
+/* The work items of the pass of order r (even, 0..12) for n samples -- a function of n and r
+ * only: T x T tiles of the sorted sample's upper block triangle
+ * (T = plugin_tile_edge(n, r): 64 for n <= 2048, else 256 R with R the rows per thread, which
+ * depends on r: the r >= 6 passes use R <= 4); diagonal tiles are full squares, weight 1;
+ * off-diagonal weight 2.  (With the A/B switch PLUGIN_PSI_TAIL=1 the last S + tiles mod S tiles
+ * are split column-wise into 4 items each.)  plugin_num_tiles: the number of items;
+ * plugin_shard_tiles: the item range [begin, end) that `rank` of `world` owns (what
+ * psi_r_shard / psi_r_shard_g process for that r, balanced to one item; an empty range for a
+ * bad rank, world or r); plugin_work_item: the pairs of one item, out5 = {row begin, row end,
+ * column begin, column end, weight} (sorted indices), 0 on success, -1 if item or r is out of
+ * range.  Host-only; no CUDA call. */
+int64_t plugin_num_tiles(int64_t n, int r);
+void plugin_shard_tiles(int64_t n, int r, int rank, int world, int64_t* begin, int64_t* end);
+int plugin_work_item(int64_t n, int r, int64_t item, int64_t* out5);
+int64_t plugin_tile_edge(int64_t n, int r);
 
 /* ---- the l-stage direct plug-in family ---- */
 

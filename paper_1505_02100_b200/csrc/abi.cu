@@ -108,7 +108,7 @@ static plugin_status run_step1(const float* d_x, int64_t n, plugin_result* d_out
 // exact pass are both launched; the device runs the one ctrl->grouped selects
 static cudaError_t pass(WS& w, int64_t n, int r, int skip, double g_host, const double* g_dev, const int32_t* status_dev,
                         int slot, int rank, int world, cudaStream_t s, PsiFin fin) {
-  const int64_t tiles = psi_work_units(n);
+  const int64_t tiles = psi_work_units(n, r);
   cudaError_t e = launch_psi(w.xs, n, r, skip, g_host, g_dev, status_dev, w.ctrl, slot, tiles * rank / world,
                              tiles * (rank + 1) / world, s, fin);
   if (e != cudaSuccess) return e;
@@ -127,17 +127,19 @@ size_t plugin_host_workspace_bytes(int64_t n) {
   return layout(n).total + align_up(sizeof(float) * (size_t)(n > 0 ? n : 1), 256);
 }
 
-int64_t plugin_num_tiles(int64_t n) { return n > 0 ? psi_work_units(n) : 0; }
+static bool valid_r(int r) { return r >= 0 && r <= 12 && !(r & 1); }
 
-int64_t plugin_tile_edge(int64_t n) { return n > 0 ? psi_tile_edge(n) : 0; }
+int64_t plugin_num_tiles(int64_t n, int r) { return n > 0 && valid_r(r) ? psi_work_units(n, r) : 0; }
 
-int plugin_work_item(int64_t n, int64_t item, int64_t* out5) {
-  if (!out5) return -1;
-  return psi_work_item(n, item, out5) ? 0 : -1;
+int64_t plugin_tile_edge(int64_t n, int r) { return n > 0 && valid_r(r) ? psi_tile_edge(n, r) : 0; }
+
+int plugin_work_item(int64_t n, int r, int64_t item, int64_t* out5) {
+  if (!out5 || !valid_r(r)) return -1;
+  return psi_work_item(n, r, item, out5) ? 0 : -1;
 }
 
-void plugin_shard_tiles(int64_t n, int rank, int world, int64_t* begin, int64_t* end) {
-  int64_t w = plugin_num_tiles(n);
+void plugin_shard_tiles(int64_t n, int r, int rank, int world, int64_t* begin, int64_t* end) {
+  int64_t w = plugin_num_tiles(n, r);
   if (world < 1 || rank < 0 || rank >= world) {
     if (begin) *begin = 0;
     if (end) *end = 0;

@@ -40,23 +40,24 @@ constexpr int64_t kFusedMaxN = 2048;
 // and the extra launches would weigh on the latency
 constexpr int64_t kGroupMinN = 32768;
 
-// rows per thread R as a function of n (tile edge T = 256 R); see DESIGN.md §5
-int psi_rows_per_thread(int64_t n);
+// rows per thread R as a function of n and the order r of the pass (tile edge T = 256 R); see
+// DESIGN.md §5
+int psi_rows_per_thread(int64_t n, int r);
 // R = 0: the small-tile mode of psi_tile.cuh (T = 64, n <= kFusedMaxN)
-inline int64_t psi_tile_edge(int64_t n) {
-  const int R = psi_rows_per_thread(n);
+inline int64_t psi_tile_edge(int64_t n, int r) {
+  const int R = psi_rows_per_thread(n, r);
   return R == 0 ? 64 : (int64_t)kPsiThreads * R;
 }
-inline int64_t psi_blocks(int64_t n) { int64_t T = psi_tile_edge(n); return (n + T - 1) / T; }
-inline int64_t psi_tiles(int64_t n) { int64_t b = psi_blocks(n); return b * (b + 1) / 2; }
+inline int64_t psi_blocks(int64_t n, int r) { int64_t T = psi_tile_edge(n, r); return (n + T - 1) / T; }
+inline int64_t psi_tiles(int64_t n, int r) { int64_t b = psi_blocks(n, r); return b * (b + 1) / 2; }
 // the pass's schedulable work items for n samples (a function of n only): whole tiles, then the
 // column quarters of the tail tiles (psi.cu); launch_psi ranges and the multi-GPU shards
 // (plugin_shard_tiles) count these.  psi_work_item: rows [out0, out1), columns [out2, out3) and
 // weight out4 of one item (host)
 constexpr int kTailSplit = 4;
-int64_t psi_work_units(int64_t n);
-int64_t psi_tail_head(int64_t n);
-bool psi_work_item(int64_t n, int64_t item, int64_t* out);
+int64_t psi_work_units(int64_t n, int r);
+int64_t psi_tail_head(int64_t n, int r);
+bool psi_work_item(int64_t n, int r, int64_t item, int64_t* out);
 
 // order-preserving float bits <-> uint32 radix key (sort.cu, fused.cu)
 __device__ __forceinline__ unsigned int bits2key(unsigned int b) {

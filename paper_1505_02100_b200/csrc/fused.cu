@@ -273,7 +273,8 @@ cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int 
 }
 
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {
-  if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n) != 0) return cudaErrorNotSupported;
+  if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n, 6) != 0 || psi_rows_per_thread(n, 4) != 0)
+    return cudaErrorNotSupported;
   static DevCache grid_cache, sm_cache;
   const int max_grid = dev_cached(grid_cache, [](int dev) {
     int occ = 0, coop = 0;

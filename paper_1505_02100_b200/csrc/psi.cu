@@ -178,9 +178,9 @@ static int64_t psi_ref_slots(int R) { return 148LL * (R >= 8 ? 2 : (R <= 2 ? PSI
 // 4x more items outweighs the shorter tail), +3% at 64K, within 1% from 128K; so items are whole
 // tiles unless PLUGIN_PSI_TAIL=1.  A function of n (and that switch) only.  Items [0, head) are
 // whole tiles.
-int64_t psi_tail_head(int64_t n) {
-  const int64_t tiles = psi_tiles(n);
-  const int R = psi_rows_per_thread(n);
+int64_t psi_tail_head(int64_t n, int r) {
+  const int64_t tiles = psi_tiles(n, r);
+  const int R = psi_rows_per_thread(n, r);
   if (R == 0) return tiles;
   const char* e = getenv("PLUGIN_PSI_TAIL");
   if (!e || e[0] != '1') return tiles;
@@ -189,15 +189,15 @@ int64_t psi_tail_head(int64_t n) {
   return tiles > tail ? tiles - tail : 0;
 }
 
-int64_t psi_work_units(int64_t n) {
+int64_t psi_work_units(int64_t n, int r) {
   if (n <= 0) return 0;
-  const int64_t tiles = psi_tiles(n), head = psi_tail_head(n);
+  const int64_t tiles = psi_tiles(n, r), head = psi_tail_head(n, r);
   return head + kTailSplit * (tiles - head);
 }
 
-bool psi_work_item(int64_t n, int64_t item, int64_t* out) {
-  if (n <= 0 || item < 0 || item >= psi_work_units(n)) return false;
-  const int64_t T = psi_tile_edge(n), nb = (n + T - 1) / T, head = psi_tail_head(n);
+bool psi_work_item(int64_t n, int r, int64_t item, int64_t* out) {
+  if (n <= 0 || item < 0 || item >= psi_work_units(n, r)) return false;
+  const int64_t T = psi_tile_edge(n, r), nb = (n + T - 1) / T, head = psi_tail_head(n, r);
   int64_t t = item, k0 = 0, kw = T;
   if (item >= head) {
     t = head + (item - head) / kTailSplit;
@@ -217,19 +217,22 @@ bool psi_work_item(int64_t n, int64_t item, int64_t* out) {
   return true;
 }
 
-int psi_rows_per_thread(int64_t n) {
+int psi_rows_per_thread(int64_t n, int r) {
   if (const char* e = getenv("PLUGIN_PSI_R")) {  // tuning override (8, 4, 2, 1; 0 = small tiles)
-    int r = atoi(e);
-    if (r == 8 || r == 4 || r == 2 || r == 1 || (r == 0 && n <= kFusedMaxN)) return r;
+    int v = atoi(e);
+    if (v == 8 || v == 4 || v == 2 || v == 1 || (v == 0 && n <= kFusedMaxN)) return v;
   }
   if (n <= kFusedMaxN) return 0;  // small tiles (T = 64): latency-bound sizes
   // the largest R whose T = 256 R tiles number at least min_tiles[R]: R = 8 needs ~28 tiles per
-  // resident CTA (296 on 148 SMs); the smaller R (3 CTAs per SM) need fewer -- measured sweep
+  // resident CTA (296 on 148 SMs); the smaller R (3-4 CTAs per SM) need fewer -- measured sweep
   // of R = 1, 2, 4 at n = 3000 ... 130000 (profiles/r01ae_tiles_sweep.txt): R = 2 wins from
-  // n ~ 16K (32 blocks), R = 4 from n ~ 65K (64 blocks)
+  // n ~ 16K (32 blocks), R = 4 from n ~ 65K (64 blocks).  Passes of order r >= 6 (7 or more FP32
+  // lane-ops per pair: the FMA pipe is busy beside MUFU) stop at R = 4: 24 warps per SM hide the
+  // longer Horner chains better than R = 8's 16 (cfg4 psi6: 0.941 vs 0.925 of the MUFU roofline;
+  // psi4 prefers R = 8: 0.962 vs 0.957; profiles/r03d_R_sweep.jsonl)
   const int cand[3] = {8, 4, 2};
   const int64_t min_blocks[3] = {128, 64, 32};
-  for (int k = 0; k < 3; ++k) {
+  for (int k = (r >= 6 ? 1 : 0); k < 3; ++k) {
     int64_t T = (int64_t)kPsiThreads * cand[k], nb = (n + T - 1) / T;
     if (nb >= min_blocks[k]) return cand[k];
   }
@@ -250,14 +253,14 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;
   psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te,
-                                                   psi_tail_head(n), fin);
+                                                   psi_tail_head(n, ORDER), fin);
   return cudaGetLastError();
 }
 
 cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_host, const double* g_dev,
                        const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end,
                        cudaStream_t s, PsiFin fin) {
-  const int R = psi_rows_per_thread(n);
+  const int R = psi_rows_per_thread(n, r);
   if (tile_end <= tile_begin)  // no tiles: the epilogue still runs (on a zero total)
     return fin.what >= 0 ? launch_finalize(fin.what, ctrl, slot, nullptr, fin.out, n, fin.g, fin.r, fin.d_psi,
                                            nullptr, s)

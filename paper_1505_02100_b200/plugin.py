@@ -85,13 +85,13 @@ def lib():
             "psi_r_shard": (i32, [i64, i32, i32, i32, P, P, P, sz, P]),
             "plugin_after_psi6": (i32, [P, P, P]),
             "plugin_after_psi4": (i32, [P, P, P]),
-            "plugin_num_tiles": (i64, [i64]),
-            "plugin_tile_edge": (i64, [i64]),
-            "plugin_work_item": (i32, [i64, i64, ctypes.POINTER(i64)]),
+            "plugin_num_tiles": (i64, [i64, i32]),
+            "plugin_tile_edge": (i64, [i64, i32]),
+            "plugin_work_item": (i32, [i64, i32, i64, ctypes.POINTER(i64)]),
             "psi_r_shard_g": (i32, [i64, d, i32, i32, i32, P, P, sz, P]),
             "plugin_prepare": (i32, [P, i64, P, sz, P]),
             "plugin_psi_from_total": (i32, [P, i64, d, i32, P, P]),
-            "plugin_shard_tiles": (None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "plugin_shard_tiles": (None, [i64, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "plugin_dpi": (i32, [P, i64, i32, P, P, sz, P]),
             "plugin_sort": (i32, [P, i64, P, P, sz, P]),
             "plugin_q32_workspace_bytes": (sz, [i64]),
@@ -385,25 +385,26 @@ def plugin_after_psi4(total: torch.Tensor, out: torch.Tensor, stream=None):
     return out
 
 
-def plugin_num_tiles(n: int) -> int:
-    return lib().plugin_num_tiles(n)
+def plugin_num_tiles(n: int, r: int) -> int:
+    """Work items of the order-r pass for n samples (tiles; a function of n and r)."""
+    return lib().plugin_num_tiles(n, r)
 
 
-def plugin_tile_edge(n: int) -> int:
-    return lib().plugin_tile_edge(n)
+def plugin_tile_edge(n: int, r: int) -> int:
+    return lib().plugin_tile_edge(n, r)
 
 
-def plugin_work_item(n: int, item: int) -> tuple[tuple[int, int], tuple[int, int], int]:
-    """The pairs of work item `item`: (row range, column range, weight) in sorted indices."""
+def plugin_work_item(n: int, r: int, item: int) -> tuple[tuple[int, int], tuple[int, int], int]:
+    """The pairs of work item `item` of the order-r pass: (row range, column range, weight)."""
     out = (ctypes.c_int64 * 5)()
-    if lib().plugin_work_item(n, item, out) != 0:
+    if lib().plugin_work_item(n, r, item, out) != 0:
         raise IndexError(f"work item {item} out of range for n={n}")
     return (out[0], out[1]), (out[2], out[3]), out[4]
 
 
-def plugin_shard_tiles(n: int, rank: int, world: int) -> tuple[int, int]:
+def plugin_shard_tiles(n: int, r: int, rank: int, world: int) -> tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
-    lib().plugin_shard_tiles(n, rank, world, ctypes.byref(b), ctypes.byref(e))
+    lib().plugin_shard_tiles(n, r, rank, world, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
 
 

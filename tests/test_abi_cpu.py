@@ -55,16 +55,26 @@ def test_workspace_sizes_monotone(L):
 
 @pytest.mark.parametrize("n", [1, 2, 255, 256, 257, 16384, 131072, 1 << 20, 4194304])
 def test_tiles_cover_triangle(L, n):
-    w = L.plugin_num_tiles(n)
-    assert w >= 1
-    for world in (1, 2, 3, 4, 8):
-        spans = [L.plugin_shard_tiles(n, r, world) for r in range(world)]
-        assert spans[0][0] == 0 and spans[-1][1] == w
-        for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
-            assert e0 == b1
-        sizes = [e - b for b, e in spans]
-        assert max(sizes) - min(sizes) <= 1           # equal-work tiles, balanced to one tile
-    assert L.plugin_shard_tiles(n, 3, 2) == (0, 0)    # invalid rank -> empty range
+    for order in (4, 6, 12):
+        w = L.plugin_num_tiles(n, order)
+        assert w >= 1
+        for world in (1, 2, 3, 4, 8):
+            spans = [L.plugin_shard_tiles(n, order, k, world) for k in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == w
+            for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
+                assert e0 == b1
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1           # equal-work tiles, balanced to one tile
+        assert L.plugin_shard_tiles(n, order, 3, 2) == (0, 0)    # invalid rank -> empty range
+    assert L.plugin_num_tiles(n, 5) == 0 and L.plugin_shard_tiles(n, 5, 0, 1) == (0, 0)  # odd r
+
+
+def test_rows_per_thread_by_order(L):
+    # the r >= 6 passes stop at R = 4 (T = 1024), the r <= 4 passes go to R = 8 (T = 2048)
+    n = 1 << 20
+    assert L.plugin_tile_edge(n, 6) == 1024 and L.plugin_tile_edge(n, 8) == 1024
+    assert L.plugin_tile_edge(n, 4) == 2048 and L.plugin_tile_edge(n, 2) == 2048
+    assert L.plugin_tile_edge(1000, 6) == L.plugin_tile_edge(1000, 4) == 64
 
 
 @pytest.mark.parametrize("n", [1, 2, 2048, 2049, 5000, 16384, 50000, 131072, 1 << 20])
@@ -72,13 +82,14 @@ def test_work_items_partition_the_triangle(n):
     # every tile's columns are covered exactly once by its items (whole, or 4 quarters), rows
     # and weights are the tile's; the items cover exactly the upper block triangle
     from paper_1505_02100_b200 import plugin as P
-    T, items = P.plugin_tile_edge(n), P.plugin_num_tiles(n)
+    order = 6 if n % 2 else 4
+    T, items = P.plugin_tile_edge(n, order), P.plugin_num_tiles(n, order)
     nb = -(-n // T)
     cover = {}
     step = max(1, items // 4000)  # large n: a deterministic sample of items plus all tail items
     idx = sorted(set(range(0, items, step)) | set(range(max(0, items - 8 * 444 * 4), items)))
     for it in idx:
-        (r0, r1), (c0, c1), w = P.plugin_work_item(n, it)
+        (r0, r1), (c0, c1), w = P.plugin_work_item(n, order, it)
         bi, bj = r0 // T, (c0 // T) if c1 > c0 else None
         assert r0 == bi * T and r1 == min(n, r0 + T) and 0 <= r0 < r1 <= n
         if bj is None:
@@ -97,7 +108,7 @@ def test_work_items_partition_the_triangle(n):
                 assert a1 == b0
             assert spans[0][0] == full[0][0] and spans[-1][1] == full[0][1]
     with pytest.raises(IndexError):
-        P.plugin_work_item(n, items)
+        P.plugin_work_item(n, order, items)
 
 
 def test_kde_workspace_sizing(L):

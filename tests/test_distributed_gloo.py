@@ -88,7 +88,7 @@ class _FakePlugin:
         return out
 
     def psi_r_shard(self, n, r, rank, world, out, partial, ws, stream=None):
-        tb, te = self.real.plugin_shard_tiles(n, rank, world)
+        tb, te = self.real.plugin_shard_tiles(n, r, rank, world)
         v = sum(t * r + 1 for t in range(tb, te)) << 70      # exercise the upper limbs too
         partial.copy_(torch.tensor(to_limbs(v), dtype=torch.int64))
         return partial
@@ -123,8 +123,7 @@ def test_plugin_h_distributed_sequencing_with_gloo(world, n):
     import __graft_entry__
     __graft_entry__.build()
     from paper_1505_02100_b200 import plugin as real
-    tiles = real.plugin_num_tiles(n)
-    want = {r: sum(t * r + 1 for t in range(tiles)) << 70 for r in (6, 4)}
+    want = {r: sum(t * r + 1 for t in range(real.plugin_num_tiles(n, r))) << 70 for r in (6, 4)}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + random.Random().randrange(2000)

@@ -255,10 +255,10 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
             part = P.new_partial()
             P.psi_r_shard(n, r, rank, world, dres, part, ws)
             got = from_limbs(part.cpu().tolist()) / 2.0 ** 64 * phi0
-            ib, ie = P.plugin_shard_tiles(n, rank, world)
+            ib, ie = P.plugin_shard_tiles(n, r, rank, world)
             ref = 0.0
             for it in range(ib, ie):        # each work item: a tile or a tail-tile quarter
-                rows, cols, w = P.plugin_work_item(n, it)
+                rows, cols, w = P.plugin_work_item(n, r, it)
                 if cols[1] > cols[0]:
                     ref += w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols)
             assert rel(got, ref) < TOL, (k, r, rank, got, ref, rel(got, ref))
@@ -560,7 +560,7 @@ def test_plugin_h_on_a_second_device(P):
 
 
 def _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t):
-    rows, cols, w = P.plugin_work_item(n, t)
+    rows, cols, w = P.plugin_work_item(n, r, t)
     return w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols) if cols[1] > cols[0] else 0.0
 
 
@@ -569,7 +569,7 @@ def _one_tile(P, n, r, t, ntiles, dres, ws):
     from paper_1505_02100_b200.distributed import from_limbs
     part = P.new_partial()
     P.psi_r_shard(n, r, t, ntiles, dres, part, ws)
-    assert P.plugin_shard_tiles(n, t, ntiles) == (t, t + 1)
+    assert P.plugin_shard_tiles(n, r, t, ntiles) == (t, t + 1)
     return from_limbs(part.cpu().tolist()) / 2.0 ** 64 / math.sqrt(2 * math.pi)
 
 
@@ -581,7 +581,7 @@ def _bandwidth_record(P, n, g_a, g_b):
 
 @pytest.mark.parametrize("n", [100000, 300000])
 def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
-    """Outliers at the sizes that select R = 4 (n = 1e5, T = 1024) and R = 8 (n = 3e5, T = 2048)
+    """Outliers at the sizes that select R = 4 (n = 1e5, T = 1024) and R = 8 (n = 3e5, r = 4: T = 2048)
     tiles: the tiles that hold them span far more than 64 bandwidths and take the wide path
     (difference first, clamped u^2, psi_tile.cuh); those tiles, the diagonal tiles at both ends and
     a middle tile, one by one against the oracle's block sums of the same pairs."""
@@ -593,13 +593,13 @@ def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
     ws = P.workspace(n)
     P.plugin_step1(xd, P.new_result(), ws)
     zs = np.sort(oracle_mod.widen(x))
-    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
-    assert T == (1024 if n == 100000 else 2048)
-    nb = -(-n // T)
-    picks = sorted({0, 1, nb - 1, nb // 2 * nb - (nb // 2) * (nb // 2 - 1) // 2,   # row 0 (outliers), mid diag
-                    ntiles - 1, ntiles - 2,                                           # last tiles
-                    (nb - 2) * nb - (nb - 2) * (nb - 3) // 2 + 1})                    # row nb-2, last column
     for r, g in ((6, 0.3), (4, 0.2)):
+        ntiles, T = P.plugin_num_tiles(n, r), P.plugin_tile_edge(n, r)
+        assert T == (2048 if (n == 300000 and r == 4) else 1024)   # R = 8 only for r <= 4
+        nb = -(-n // T)
+        picks = sorted({0, 1, nb - 1, nb // 2 * nb - (nb // 2) * (nb // 2 - 1) // 2,   # row 0 (outliers), mid diag
+                        ntiles - 1, ntiles - 2,                                           # last tiles
+                        (nb - 2) * nb - (nb - 2) * (nb - 3) // 2 + 1})                    # row nb-2, last column
         dres = _bandwidth_record(P, n, g, g)
         for t in picks:
             got = _one_tile(P, n, r, t, ntiles, dres, ws)
@@ -607,13 +607,13 @@ def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
             assert math.isfinite(got)
             # relative 1e-5; terms below the fp32 range (e^(-u^2/2) < 2^-126: the far tiles) are
             # +0 on the GPU, so an absolute T^2 2^-100 is allowed on top
-            assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (n, r, t, P.plugin_work_item(n, t), got, ref)
+            assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (n, r, t, P.plugin_work_item(n, r, t), got, ref)
 
 
 @pytest.mark.parametrize("r", [8, 12])
 def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
-    """The general-r pass (He_r phi, the plugin_dpi family) at BASELINE config 4 (R = 8 tiles,
-    where test_gpu_dpi's full-oracle cases do not reach): sampled tiles against the oracle."""
+    """The general-r pass (He_r phi, the plugin_dpi family) at BASELINE config 4 (R = 4 tiles at
+    this size, where test_gpu_dpi's full-oracle cases do not reach): sampled tiles against the oracle."""
     x = inputs.config_data(4)
     n = x.size
     xd = torch.from_numpy(x).cuda()
@@ -622,13 +622,13 @@ def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
     zs = np.sort(oracle_mod.widen(x))
     sigma = oracle_mod.step1(x)["sigma"]
     g = 0.35 * sigma
-    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
+    ntiles, T = P.plugin_num_tiles(n, r), P.plugin_tile_edge(n, r)
     nb = -(-n // T)
     dres = _bandwidth_record(P, n, g, g)
     for t in (0, 5, nb + 3, ntiles // 2, ntiles // 2 + 1, ntiles - 3, ntiles - 1):
         got = _one_tile(P, n, r, t, ntiles, dres, ws)
         ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
-        assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, P.plugin_work_item(n, t), got, ref)
+        assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, P.plugin_work_item(n, r, t), got, ref)
 
 
 @pytest.mark.parametrize("case", ["cfg2", "ties_grouped", "small"])

@@ -53,13 +53,12 @@ def main():
         P.psi_r_shard(n, 6, 0, 1, out, part, ws)
         P.plugin_after_psi6(part, out)
         torch.cuda.synchronize()
-        row = {"n": n, "units": P.plugin_num_tiles(n), "R_env": os.environ.get("PLUGIN_PSI_R", ""),
+        row = {"n": n, "units": P.plugin_num_tiles(n, 6), "R_env": os.environ.get("PLUGIN_PSI_R", ""),
                "lib": os.path.basename(P.LIB_PATH)}
-        if hasattr(P.lib(), "plugin_tile_edge"):
-            row["T"] = P.plugin_tile_edge(n)
+        row["T6"], row["T4"] = P.plugin_tile_edge(n, 6), P.plugin_tile_edge(n, 4)
         # an empty shard (rank 0 of units + 1 ranks owns [0, 0)) runs only the export kernel
-        world = P.plugin_num_tiles(n) + 1
-        assert P.plugin_shard_tiles(n, 0, world) == (0, 0)
+        world = P.plugin_num_tiles(n, 6) + 1
+        assert P.plugin_shard_tiles(n, 6, 0, world) == (0, 0)
         export = graph_us(lambda: P.psi_r_shard(n, 6, 0, world, out, part, ws))
         row["export_us"] = round(export, 2)
         pairs = n * (n - 1) / 2

@@ -22,7 +22,7 @@ def main():
         ws = P.workspace(n, x.device)
         out = P.new_result(x.device)
         P.plugin_step1(x, out, ws)
-        row = {"n": n, "units": P.plugin_num_tiles(n), "T": P.plugin_tile_edge(n),
+        row = {"n": n, "units6": P.plugin_num_tiles(n, 6), "T6": P.plugin_tile_edge(n, 6), "T4": P.plugin_tile_edge(n, 4),
                "R_env": os.environ.get("PLUGIN_PSI_R", "")}
         for r in (6, 4):
             ts = []

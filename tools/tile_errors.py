@@ -45,7 +45,7 @@ def main():
     res.status, res.n, res.g1, res.g2 = 0, n, g, g
     dres = torch.frombuffer(bytearray(bytes(res)), dtype=torch.uint8).cuda()
     zs = np.sort(oracle.widen(x))
-    ntiles, T = P.plugin_num_tiles(n), P.plugin_tile_edge(n)
+    ntiles, T = P.plugin_num_tiles(n, r), P.plugin_tile_edge(n, r)
     nb = -(-n // T)
     off = lambda b: b * nb - b * (b - 1) // 2  # noqa: E731
     picks = set(off(b) for b in range(nb)) | set(off(b) + 1 for b in range(nb - 1))
