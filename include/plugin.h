@@ -87,7 +87,7 @@ size_t plugin_workspace_bytes(int64_t n);
  *   d_out : device plugin_result, written when the stream reaches the end of the call
  * Launches: a sort of X into the workspace (summation order only), the Step I reduction,
  * the Step IV pass, its finalize (psi6, g2), the Step VI pass, its finalize (psi4, h);
- * for n <= 2048 all of it is one cooperative launch with the same results (plugin_h_ex).
+ * for n <= 2048 all of it is one thread-block-cluster launch with the same results (plugin_h_ex).
  */
 plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
                        void* d_ws, size_t ws_bytes, void* stream);
@@ -98,7 +98,7 @@ plugin_status plugin_h(const float* d_x, int64_t n, plugin_result* d_out,
  * result is bit-identical to plugin_h; only the work changes (the
  * headline pair rate is always measured without it).  Unknown bits -> PLUGIN_E_INVALID. */
 #define PLUGIN_SKIP_UNDERFLOW 1u
-/* PLUGIN_MULTI_KERNEL: for n <= 2048 plugin_h runs the whole algorithm in one cooperative
+/* PLUGIN_MULTI_KERNEL: for n <= 2048 plugin_h runs the whole algorithm in one cluster
  * launch (sort, Step I, both passes and the scalar steps; bit-identical to the multi-kernel
  * sequence); this flag forces the multi-kernel sequence instead (testing, timing). */
 #define PLUGIN_MULTI_KERNEL 2u
@@ -116,7 +116,7 @@ plugin_status plugin_h_batch(const float* d_x, const int64_t* d_offsets, int cou
                              unsigned int flags, void* stream);
 
 /* plugin_h as a CUDA graph, for repeated runs on the same buffers (the launch latency of the
- * kernel sequence -- or of the one cooperative launch for n <= 2048 -- is paid once at
+ * kernel sequence -- or of the one cluster launch for n <= 2048 -- is paid once at
  * creation).  plugin_graph_create captures plugin_h_ex(d_x, n, d_out, flags, d_ws, ws_bytes)
  * with its arguments fixed: the caller keeps d_x, d_out and d_ws alive and may change the
  * CONTENTS of d_x between launches.  The handle (host memory, owned by the caller) is freed by

@@ -41,7 +41,7 @@ Layout layout(int64_t n) {
   L.result = off;
   off = align_up(off + sizeof(plugin_result), 256);
   L.fused = off;
-  off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid + 256, 256);  // fused.cu partials (32 KB) + timing slots
+  off = align_up(off + sizeof(Fx128) * 2 * kFusedMaxGrid + 256, 256);  // fused.cu sort scratch (32 KB) + timing slots
   // group.cu: per-4096-chunk distinct counts, then at most n/4 distinct values and run starts (+1)
   const size_t nn = (size_t)(n > 0 ? n : 1);
   L.grp_heads = off;
@@ -174,7 +174,7 @@ plugin_status plugin_h_ex(const float* d_x, int64_t n, plugin_result* d_out, uns
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (n <= kFusedMaxN && !(flags & PLUGIN_MULTI_KERNEL)) {
-    // small n: the whole algorithm in one cooperative launch (fused.cu), bit-identical
+    // small n: the whole algorithm in one thread-block-cluster launch (fused.cu), bit-identical
     Fx128* parts = reinterpret_cast<Fx128*>(static_cast<char*>(d_ws) + w.L.fused);
     e = launch_fused(d_x, n, skip, d_out, parts, s);
     if (e == cudaSuccess) return PLUGIN_OK;

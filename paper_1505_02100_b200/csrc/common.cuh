@@ -144,8 +144,9 @@ constexpr double kSkipU = 13.25;
 cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* total, plugin_result* out,
                             int64_t n, double g_host, int r, double* d_psi, plugin_fx128* d_limbs,
                             cudaStream_t s);
-// the whole of Alg. 1 in one cooperative launch for n <= kFusedMaxN (fused.cu); parts holds
-// 2 * kFusedMaxGrid Fx128.  Returns cudaErrorNotSupported if the path does not apply.
+// the whole of Alg. 1 in one thread-block-cluster launch for n <= kFusedMaxN (fused.cu); parts: 32 KB
+// of workspace scratch (the sort's runs and ascending array; 2 * kFusedMaxGrid Fx128 in size).
+// Returns cudaErrorNotSupported if the path does not apply (no cluster of 8 can be scheduled).
 constexpr int kFusedMaxGrid = 1024;
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s);
 // many samples of 2 <= n_b <= kFusedMaxN, one CTA each (fused.cu): offsets[count + 1] on the device

@@ -1,18 +1,8 @@
-// fused.cu -- the whole of Algorithm 1 in ONE cooperative launch for
-// small samples (n <= kFusedMaxN = 2048, which covers the paper's own workloads n = 128..1024
-// of Tables 2-4 and BASELINE config 1).  At these sizes a pass is ~0.1-4 us of arithmetic, so
-// the 20 launches of the multi-kernel path dominate; here they become one launch and two
-// grid-wide barriers.
-//
-// Every CTA loads X into shared memory, sorts it (bitonic sort on the radix keys of sort.cu:
-// the same unique ascending array), and computes Step I and Steps II-III redundantly with the
-// reduction tree of step1_kernel (steps.cuh), so every CTA holds the same g1 without
-// communication.  The psi pass tiles (psi_tile.cuh, T = 256) are dealt round-robin to the
-// CTAs; each CTA writes its exact 128-bit fixed-point partial to its own slot, the grid
-// synchronises, and every CTA adds the slots (integer addition: order-free) and finalises
-// Step V identically; the Step VI pass follows the same way and CTA 0 writes the result.
-// Every tile sum, the fixed-point total and the scalar chain are computed by the same device
-// code as the multi-kernel path, so the result is bit-identical to it (tested).
+// fused.cu -- the whole of Algorithm 1 in ONE launch for small samples
+// (n <= kFusedMaxN = 2048, which covers the paper's own workloads n = 128..1024 of Tables 2-4 and
+// BASELINE config 1), and many small samples in one launch (plugin_h_batch).  At these sizes a
+// pass is ~0.1-4 us of arithmetic, so the launches of the multi-kernel path dominate; here they
+// become one thread-block cluster that communicates through distributed shared memory.
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -26,15 +16,15 @@ namespace cg = cooperative_groups;
 namespace plg {
 
 // -DPLUGIN_FUSED_TIMING: CTA 0 records %globaltimer (ns) at the phase boundaries into the
-// workspace after the partials (tools/fused_phases.py reads them); off in the product build
+// workspace (tools/fused_phases.py reads them); off in the product build
 #ifdef PLUGIN_FUSED_TIMING
-#define FT_MARK(k)                                                                   \
-  do {                                                                               \
-    if ((blockIdx.x == 0 || (k) >= 7) && threadIdx.x == 0) { /* 7, 8: the last CTA */ \
-      unsigned long long t;                                                          \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                          \
-      reinterpret_cast<unsigned long long*>(parts + 2 * kFusedMaxGrid)[k] = t;       \
-    }                                                                                \
+#define FT_MARK(k)                                                             \
+  do {                                                                         \
+    if (crank == 0 && threadIdx.x == 0) {                                      \
+      unsigned long long t;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                    \
+      reinterpret_cast<unsigned long long*>(parts + 2 * kFusedMaxGrid)[k] = t; \
+    }                                                                          \
   } while (0)
 #else
 #define FT_MARK(k) \
@@ -42,14 +32,7 @@ namespace plg {
   } while (0)
 #endif
 
-__device__ __forceinline__ Fx128 ldcg_fx(const Fx128* p) {
-  Fx128 r;
-  r.lo = __ldcg(&p->lo);
-  r.hi = __ldcg(&p->hi);
-  return r;
-}
-
-// Every CTA of a single-sample launch (and each CTA of a batch): the sorted sample in shared
+// Each CTA of a batch (plugin_batch_kernel): the sorted sample in shared
 // memory (padded to nsx with its largest value) and Steps I-III in res, with the reduction tree
 // of step1_kernel.  Contains __syncthreads().
 __device__ __forceinline__ void cta_prologue(const float* __restrict__ x, int64_t n, int nsx, float* xsm,
@@ -93,90 +76,219 @@ __device__ __forceinline__ void cta_prologue(const float* __restrict__ x, int64_
   __syncthreads();
 }
 
-template <int R>
-__global__ void __launch_bounds__(kPsiThreads)
-plugin_fused_kernel(const float* __restrict__ x, int64_t n, int nsx, int skip, plugin_result* out, Fx128* parts) {
-  extern __shared__ __align__(16) float xsm[];  // nsx floats: the sorted sample, padded; then sort scratch
-  __shared__ double sh1[8], sh2[8], red[kPsiThreads / 32];
-  __shared__ int sh_bad[8];
-  __shared__ double p1[2 * 8];
-  __shared__ plugin_result res;
-  __shared__ Fx128 fx_red[kPsiThreads / 32];
-  static_assert(R == 0, "the fused path uses the small tiles of psi_tile.cuh");
-  constexpr int T = kPsiSmallT;
-  const int tid = threadIdx.x;
+// ---- the single launch for small n: one thread-block cluster ------------------------------------
+// C = 16 CTAs of 1024 threads (one cluster; 8 if the device refuses 16), distributed shared memory
+// instead of global partials and a cooperative grid barrier:
+//   sort  every CTA reads the n keys (blocksort_key, the order of sort.cu); CTA c ranks its slice of
+//         ceil(n / C) keys against all n (rank = keys below + equal keys at lower index: unique) and
+//         writes each value to its rank in a workspace array; after the cluster barrier every CTA
+//         reads the whole array back: THE ascending array (the one the radix and block sorts give;
+//         4-byte scattered stores to global memory and one coalesced reload are cheaper than
+//         scattering into 16 CTAs' shared memory, measured);
+//   I-III every CTA, redundantly, with step1_kernel's reduction tree (steps.cuh): the same g1 as the
+//         multi-kernel path, no communication;
+//   IV/VI the 64 chunks of each T = 64 tile (psi_chunk64: a row against the tile's 64 columns)
+//         are spread over the cluster's threads; each chunk is a 128-bit fixed-point integer, a CTA
+//         adds its chunks, and the CTA partials go to every CTA's shared memory (pass 6) or to CTA
+//         0's (pass 4); cluster barrier; the receivers add them (integer: order-free) and finalise
+//         Step V (every CTA, identically) or Step VII (CTA 0, which writes the record).
+// The chunks, their integer total and the scalar chain are computed by the same device code as the
+// multi-kernel path (psi_small_kernel, step1_kernel, finalize_pass), so the result is bit-identical to
+// it (tested).
+constexpr int kFusedThreads = 1024;
+constexpr int kFusedClusterMax = 16;
 
+// shared memory of the cluster kernel for n samples: per row 2^-p_i (double), the sorted sample
+// padded to whole tiles with its largest value, p_i and the scale dither k_i (float); the C sorted
+// runs of the sort (uint64, C (m + 1) <= n + 5 C); the tile table (ushort)
+constexpr int kFusedSliceMax = (int)(kFusedMaxN / 8) + 4;  // slice length at the smallest cluster (8)
+// up to this n the sort counts each key against all n (one exchange); above, C sorted slices are
+// merged by binary search (two exchanges, O(n log n)); measured: the counting sort takes 1.4 / 3.6 us
+// at n = 128 / 1024 against 3.0 / 4.0 for the merge, 10.2 against 5.0 at n = 2048
+constexpr int64_t kFusedCountMaxN = 1024;
+__host__ __device__ inline int fused_nsx(int64_t n) { return (int)((n + kPsiSmallT - 1) / kPsiSmallT * kPsiSmallT); }
+__host__ __device__ inline int fused_tiles(int64_t n) { const int nb = fused_nsx(n) / kPsiSmallT; return nb * (nb + 1) / 2; }
+__host__ __device__ inline int fused_runs(int64_t n) { return (int)n + 5 * kFusedClusterMax; }
+inline size_t fused_smem(int64_t n) {
+  return (size_t)fused_nsx(n) * 20 + (size_t)fused_runs(n) * 8 + (size_t)fused_tiles(n) * 2;
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1)
+plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_result* out, Fx128* parts) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int nsx = fused_nsx(n), n4 = (int)((n + 3) / 4);
+  double* comp = reinterpret_cast<double*>(fsm);
+  float* xsm = reinterpret_cast<float*>(fsm + (size_t)nsx * 8);
+  float* rph = xsm + nsx;
+  float* rsc = rph + nsx;
+  unsigned long long* runs = reinterpret_cast<unsigned long long*>(rsc + nsx);  // C sorted runs of composites
+  unsigned short* ttab = reinterpret_cast<unsigned short*>(runs + fused_runs(n));
+  __shared__ Fx128 fxred[kFusedThreads / 32];
+  __shared__ unsigned long long sk[kFusedSliceMax];  // this CTA's slice of composites
+  __shared__ Fx128 cparts[2][kFusedClusterMax];  // the CTAs' pass partials, written by their CTAs
+  __shared__ double sh1[8], sh2[8], p1[2 * 8];
+  __shared__ int sh_bad[8];
+  __shared__ plugin_result res;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
   FT_MARK(0);
-  cta_prologue(x, n, nsx, xsm, &res, sh1, sh2, sh_bad, p1);
-  FT_MARK(1);
-  const float xpad = xsm[n - 1];
-  FT_MARK(2);
-  // Steps IV/V and VI/VII
-  cg::grid_group grid = cg::this_grid();
-  const int64_t nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
-  // pass 4's arrival counter (after the partials and the timing slots); zeroed by CTA 0 before
-  // the grid barrier of pass 6, incremented only after it
-  unsigned int* arrive = reinterpret_cast<unsigned int*>(parts + 2 * kFusedMaxGrid) + 32;
-  if (blockIdx.x == 0 && tid == 0) *arrive = 0u;
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool ok = res.status == PLUGIN_OK;  // the same in every CTA
-    if (ok) {
-      const float s = __double2float_rn(1.0 / (pass == 0 ? res.g1 : res.g2));
-      Fx128 acc = {0ull, 0ll};
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        int64_t bi, bj;
-        tile_coords(t, nb, bi, bj);
-        const int64_t i0 = bi * T, j0 = bj * T;
-        if (skip && bi != bj &&
-            ((double)xsm[j0] - (double)xsm[i0 + T - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
-          continue;  // all terms exactly zero (psi.cu); uniform across the CTA
-        const int jcount = (int)((n - j0) < T ? (n - j0) : T);
-        const double w = (bi == bj) ? 1.0 : 2.0;
-        const double tt = (pass == 0) ? psi_tile_sum_small<6, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red)
-                                      : psi_tile_sum_small<4, false>(xsm + j0, xsm, n, i0, jcount, s, xpad, w, red);
-        if (tid == 0) fx_add(acc, fx_from_double(tt));
-      }
-      if (tid == 0) parts[pass * gridDim.x + blockIdx.x] = acc;
-    }
-    FT_MARK(3 + 3 * pass);
-    if (pass == 0) {
-      grid.sync();  // every CTA needs g2 from the whole Step IV sum
-    } else {
-      // Step VI: only the last CTA to arrive reduces and finalises (threadfence pattern): no
-      // second grid barrier
-      __shared__ bool last;
-      if (tid == 0) {
-        __threadfence();
-        last = (atomicAdd(arrive, 1u) == gridDim.x - 1);
-      }
-      __syncthreads();
-      if (!last) return;
-      __threadfence();
-    }
-    FT_MARK(4 + 3 * pass);
-    if (ok) {
-      // the partials: in parallel over the threads (independent L2 loads), then a 128-bit
-      // shuffle / shared-memory reduction -- integer addition, so any order gives the same total
-      Fx128 tot = {0ull, 0ll};
-      for (unsigned int b = tid; b < gridDim.x; b += kPsiThreads) fx_add(tot, ldcg_fx(parts + pass * gridDim.x + b));
-      for (int o = 16; o; o >>= 1) {
-        Fx128 other;
-        other.lo = __shfl_xor_sync(0xffffffffu, tot.lo, o);
-        other.hi = __shfl_xor_sync(0xffffffffu, tot.hi, o);
-        fx_add(tot, other);
-      }
-      if ((tid & 31) == 0) fx_red[tid >> 5] = tot;
-      __syncthreads();
-      if (tid == 0) {
-        Fx128 all = {0ull, 0ll};
-        for (int w = 0; w < kPsiThreads / 32; ++w) fx_add(all, fx_red[w]);
-        finalize_pass(pass, fx_to_double(all), n, &res);
-      }
-      __syncthreads();
-    }
-    FT_MARK(5 + 3 * pass);
+
+  // ---- sort: C sorted slices, merged by rank ----
+  // CTA crank takes the keys [lo, lo + mm) of X as composites (key << 32) | index (unique: equal keys
+  // are ordered by index), ranks them within the slice (P = 2^lp lanes per key) and writes the
+  // sorted slice, padded with ~0, to run crank of the workspace; after a cluster barrier every CTA
+  // loads all C runs, ranks its own keys in each by binary search (rank = sum over the runs) and
+  // writes the values to their ranks (srt); after a second barrier every CTA reads the ascending
+  // array back (THE ascending array: the one the radix and block sorts give).  Global scratch plus
+  // cluster barriers: scattered 4-byte stores into 16 CTAs' shared memory were slower (measured).
+  const unsigned int* xb = reinterpret_cast<const unsigned int*>(x);
+  const int m = (int)((n + C - 1) / C + 3) & ~3;  // slice length, a multiple of 4 (<= kFusedSliceMax)
+  const int lo = crank * m, mm = (int)n - lo < m ? ((int)n - lo > 0 ? (int)n - lo : 0) : m;
+  int mp = 1;  // m rounded up to a power of two
+  while (mp < m) mp <<= 1;
+  int lp = 5;  // P = min(32, 1024 / mp) lanes per key
+  while (lp > 0 && (mp << lp) > kFusedThreads) --lp;
+  const bool counting = n <= kFusedCountMaxN;
+  if (counting) {  // all n composites (runs[] holds them); the slice is a part of them
+    for (int i = tid; i < (int)n; i += kFusedThreads)
+      runs[i] = ((unsigned long long)blocksort_key(__ldg(xb + i)) << 32) | (unsigned int)i;
+  } else {
+    for (int k = tid; k < m; k += kFusedThreads)
+      sk[k] = k < mm ? ((unsigned long long)blocksort_key(__ldg(xb + lo + k)) << 32) | (unsigned int)(lo + k) : ~0ull;
   }
-  // the last CTA of pass 4 (every CTA holds the same record up to here)
+  if (tid == 0) init_result(&res, n);
+  // pass-independent row tables and the tile table (tile t -> block row, block column)
+  const int64_t nb = nsx / kPsiSmallT, tiles = nb * (nb + 1) / 2;
+  for (int i = tid; i < nsx; i += kFusedThreads) {
+    rph[i] = row_phase(i);
+    rsc[i] = (float)row_scale_offset(i, scale_dither_amp(n));  // k_i of dithered_scale
+    comp[i] = row_comp(i);
+  }
+  for (int t = tid; t < tiles; t += kFusedThreads) {
+    int64_t bi, bj;
+    tile_coords(t, nb, bi, bj);
+    ttab[t] = (unsigned short)((bi << 8) | bj);
+  }
+  __syncthreads();
+  FT_MARK(1);
+  unsigned long long* grun = reinterpret_cast<unsigned long long*>(parts);            // C runs of m
+  float* srt = reinterpret_cast<float*>(grun + kFusedMaxN + 4 * kFusedClusterMax);  // the ascending array
+  const int ks = tid >> lp, part = tid & ((1 << lp) - 1);
+  if (counting) {
+    // small n: every CTA holds all n composites and counts those below each of its keys (P lanes
+    // per key, over the composites q = part (mod P))
+    const unsigned long long* key = runs;
+    FT_MARK(2);
+    unsigned int cnt = 0;
+    const unsigned long long ki = ks < mm ? key[lo + ks] : ~0ull;
+    if (ks < mm) {
+#pragma unroll 4
+      for (int q = part; q < (int)n; q += 1 << lp) cnt += key[q] < ki;
+    }
+    for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
+  } else {
+    const bool own = ks < m;
+    const unsigned long long ki = own ? sk[ks] : ~0ull;
+    {
+      unsigned int cnt = 0;
+      for (int q = part; q < m; q += 1 << lp) cnt += sk[q] < ki;
+      for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      // pads (~0, all equal) keep their slots after the mm real keys
+      if (own && part == 0) grun[lo + (ks < mm ? (int)cnt : ks)] = ki;
+    }
+    cluster.sync();  // release / acquire at cluster scope: every run is in the workspace
+    // runs at a stride of m + 1 composites in shared memory: the P lanes of a key search P different
+    // runs in lockstep, and an even stride would put them all on the same banks
+    for (int e = tid; e < C * m; e += kFusedThreads) {
+      const int r = e / m;
+      runs[e + r] = __ldcg(grun + e);
+    }
+    __syncthreads();
+    FT_MARK(2);
+    unsigned int cnt = 0;
+    if (ks < mm) {
+      for (int r = part; r < C; r += 1 << lp) {  // composites below ki in run r (pads never count)
+        const unsigned long long* run = runs + r * (m + 1);
+        int pos = 0;
+        for (int step = mp; step >= 1; step >>= 1)
+          if (pos + step <= m && run[pos + step - 1] < ki) pos += step;
+        cnt += (unsigned int)pos;
+      }
+    }
+    for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
+  }
+  cluster.sync();  // every value is at its rank
+  for (int q = tid; q < n4; q += kFusedThreads)
+    reinterpret_cast<float4*>(xsm)[q] = __ldcg(reinterpret_cast<const float4*>(srt) + q);
+  __syncthreads();
+  FT_MARK(3);
+
+  // ---- Steps I-III ----
+  const float xpad = xsm[n - 1];
+  for (int i = (int)n + tid; i < nsx; i += kFusedThreads) xsm[i] = xpad;
+  const int nb1 = step1_grid(n);
+  const double K = (double)xsm[0];
+  int bad = 0;
+  for (int b = 0; b < nb1; ++b) {
+    double a, q;
+    int bb;
+    step1_block(xsm, n, K, b, nb1, sh1, sh2, sh_bad, a, q, bb);
+    if (tid == 0) { p1[2 * b] = a; p1[2 * b + 1] = q; bad |= bb; }
+  }
+  FT_MARK(4);
+  __syncthreads();
+  if (tid < 32) {
+    double a, q;
+    step1_total<false>(p1, nb1, a, q);
+    if (tid == 0) step1_epilogue(a, q, n, K, bad != 0, &res);
+  }
+  __syncthreads();
+  FT_MARK(5);
+
+  // ---- Steps IV/V and VI/VII ----
+  // chunk c = 64 t + (row of tile t), dealt to the cluster's warps 32 at a time round-robin over the
+  // CTAs (warp w of CTA crank: chunks 32 (C w + crank) + lane, then + 32 C 32, ...)
+  const int nchunks = (int)tiles * kPsiSmallT;
+  const int cfirst = 32 * (C * (tid >> 5) + crank) + (tid & 31);
+  for (int pass = 0; pass < 2; ++pass) {
+    Fx128 acc = {0ull, 0ll};
+    if (res.status == PLUGIN_OK) {  // the same record in every CTA: uniform
+      const float s = __double2float_rn(1.0 / (pass == 0 ? res.g1 : res.g2));
+      const float ulp = dither_ulp(s);
+      for (int c = cfirst; c < nchunks; c += C * kFusedThreads) {
+        const int t = c >> 6;
+        const int bi = ttab[t] >> 8, bj = ttab[t] & 255;
+        const int i0 = bi * kPsiSmallT, j0 = bj * kPsiSmallT, i = i0 + (c & (kPsiSmallT - 1));
+        if (i >= n) continue;  // padding row
+        if (skip && bi != bj &&
+            ((double)xsm[j0] - (double)xsm[i0 + kPsiSmallT - 1]) * (double)s * (1.0 - 1e-5) > kSkipU)
+          continue;  // all terms exactly zero (psi.cu)
+        const int jcount = (int)((n - j0) < kPsiSmallT ? (n - j0) : kPsiSmallT);
+        const float si = __fmaf_rn(rsc[i], ulp, s);  // = dithered_scale(s, i, n)
+        const double w = (bi == bj) ? 1.0 : 2.0;
+        fx_add(acc, pass == 0 ? psi_chunk64<6, false>(xsm + j0, jcount, xsm[i], rph[i], si, comp[i], w)
+                              : psi_chunk64<4, false>(xsm + j0, jcount, xsm[i], rph[i], si, comp[i], w));
+      }
+    }
+    FT_MARK(6 + 4 * pass);
+    const Fx128 cta = block_sum_fx<kFusedThreads>(acc, fxred);  // valid in warp 0
+    FT_MARK(7 + 4 * pass);
+    // pass 6: to every CTA (each finalises Step V); pass 4: to CTA 0
+    if (tid < (pass == 0 ? C : 1)) cluster.map_shared_rank(&cparts[pass][0], tid)[crank] = cta;
+    cluster.sync();
+    FT_MARK(8 + 4 * pass);
+    if (pass == 1 && crank != 0) return;  // nothing reads this CTA's shared memory any more
+    if (tid == 0 && res.status == PLUGIN_OK) {
+      Fx128 tot = {0ull, 0ll};
+      for (int r = 0; r < C; ++r) fx_add(tot, cparts[pass][r]);
+      finalize_pass(pass, fx_to_double(tot), n, &res);
+    }
+    __syncthreads();
+    FT_MARK(9 + 4 * pass);
+  }
   if (tid == 0) *out = res;
 }
 
@@ -272,33 +384,53 @@ cudaError_t launch_batch(const float* x, const int64_t* offsets, int count, int 
   return cudaGetLastError();
 }
 
+// cluster size of the single launch on this device: 16 (non-portable) if it can be scheduled, else
+// 8, else 0 (path unavailable); PLUGIN_FUSED_CLUSTER=8 forces 8 (A/B)
+static int fused_cluster_size(int dev) {
+  (void)dev;
+  cudaFuncSetAttribute(plugin_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(plugin_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(kFusedMaxN));
+  const char* e = getenv("PLUGIN_FUSED_CLUSTER");
+  const int first = (e && atoi(e) == 8) ? 1 : 0;
+  const int cand[2] = {16, 8};
+  for (int k = first; k < 2; ++k) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cand[k];
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cand[k]);
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = fused_smem(kFusedMaxN);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, plugin_cluster_kernel, &cfg) == cudaSuccess && nc > 0) return cand[k];
+    (void)cudaGetLastError();
+  }
+  return 0;
+}
+
 cudaError_t launch_fused(const float* x, int64_t n, int skip, plugin_result* out, Fx128* parts, cudaStream_t s) {
   if (n < 2 || n > kFusedMaxN || psi_rows_per_thread(n, 6) != 0 || psi_rows_per_thread(n, 4) != 0)
     return cudaErrorNotSupported;
-  static DevCache grid_cache, sm_cache;
-  const int max_grid = dev_cached(grid_cache, [](int dev) {
-    int occ = 0, coop = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plugin_fused_kernel<0>, kPsiThreads,
-                                                  sizeof(float) * 2 * kBlockSortN);
-    const int g = coop ? device_sms(dev) * occ : 0;
-    return g > kFusedMaxGrid ? kFusedMaxGrid : g;
-  });
-  if (max_grid <= 0) return cudaErrorNotSupported;
-  const int64_t T = kPsiSmallT, nb = (n + T - 1) / T, tiles = nb * (nb + 1) / 2;
-  int nsx = (int)(nb * T > kBlockSortN ? nb * T : kBlockSortN);  // cta_sort2048 writes 2048 positions
-  // one CTA per SM at most: every CTA sorts its own copy of X, so more CTAs than SMs add no speed
-  const int sms = dev_cached(sm_cache, device_sms);
-  int grid = (int)(tiles < max_grid ? tiles : max_grid);
-  if (grid > sms) grid = sms;
-  if (const char* e = getenv("PLUGIN_FUSED_GRID")) {  // A/B only: fewer CTAs (cheaper barriers)
-    const int g = atoi(e);
-    if (g >= 1 && g < grid) grid = g;
-  }
-  size_t smem = sizeof(float) * ((size_t)nsx + kBlockSortN);  // sample + sort scratch
-  void* args[] = {(void*)&x, (void*)&n, (void*)&nsx, (void*)&skip, (void*)&out, (void*)&parts};
-  return cudaLaunchCooperativeKernel((const void*)plugin_fused_kernel<0>, dim3(grid), dim3(kPsiThreads), args, smem,
-                                     s);
+  static DevCache cl_cache;
+  const int C = dev_cached(cl_cache, fused_cluster_size);
+  if (C <= 0) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = fused_smem(n);
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, plugin_cluster_kernel, x, n, skip, out, parts);
 }
 
 }  // namespace plg

@@ -37,19 +37,49 @@
 
 namespace plg {
 
+// a pass CTA's exact partial into the slot; with a PsiFin, the last CTA to finish runs the pass's
+// epilogue (threadfence reduction pattern) and resets the slot for a later pass on the same
+// workspace.  cta_acc valid in thread 0; called by every thread; last: a shared flag.
+__device__ __forceinline__ void psi_cta_done(Fx128 cta_acc, Ctrl* ctrl, int slot, const PsiFin& fin, int64_t n,
+                                             bool* last) {
+  const int tid = threadIdx.x;
+  unsigned long long* g_lo = &ctrl->acc[slot].lo;
+  unsigned long long* g_hi = reinterpret_cast<unsigned long long*>(&ctrl->acc[slot].hi);
+  if (tid == 0 && (cta_acc.lo != 0ull || cta_acc.hi != 0ll)) {
+    unsigned long long old = atomicAdd(g_lo, cta_acc.lo);
+    unsigned long long carry = (old + cta_acc.lo < old) ? 1ull : 0ull;
+    atomicAdd(g_hi, (unsigned long long)cta_acc.hi + carry);
+  }
+  if (fin.what < 0) return;
+  if (tid == 0) {
+    __threadfence();
+    *last = (atomicAdd(&ctrl->psi_done[slot], 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!*last || tid != 0) return;
+  __threadfence();
+  Fx128 total;
+  total.lo = atomicExch(g_lo, 0ull);
+  total.hi = (long long)atomicExch(g_hi, 0ull);
+  ctrl->tile_counter[slot] = 0ull;
+  ctrl->psi_done[slot] = 0u;
+  finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
+}
+
 // min resident CTAs per SM for the register budget: R=8 -> 2 (<=128 regs), R=4 -> 3 (<=80 regs), R<=2 -> 4 (<=64)
 #ifndef PSI_OCC_R12
 #define PSI_OCC_R12 4  // R = 1, 2: <= 64 registers, no spills; 1-3% over 3 CTAs/SM at n = 12K..65K (profiles/r02p_ab_occ.jsonl)
 #endif
 template <int R>
-struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R == 0 ? 4 : (R <= 2 ? PSI_OCC_R12 : 3)); };
+struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R <= 2 ? PSI_OCC_R12 : 3); };
 
 template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, int64_t head,
            PsiFin fin) {
-  constexpr int T = (R == 0) ? kPsiSmallT : kPsiThreads * R;
+  static_assert(R >= 1, "R = 0 (small tiles) runs psi_small_kernel");
+  constexpr int T = kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
@@ -104,17 +134,13 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       __syncthreads();
       continue;
     }
-    // tile centre (R >= 1, PSI_CENTER, not wide): psi_tile_centre makes every staged x_j - cen
-    // exact; decided on the whole tile, so the quarters of a tile agree
-    float cen = 0.f;
-    bool wide = false;
-    if constexpr (R > 0) {
-      // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jtile - 1]]
-      const float a = __ldg(xs + i0), b = __ldg(xs + (i0 + T < n ? i0 + T : n) - 1);
-      const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jtile - 1);
-      wide = psi_tile_wide(a, b, p, q, s);
-      if (PSI_CENTER && !wide) cen = psi_tile_centre(a, q);
-    }
+    // tile centre (PSI_CENTER, not wide): psi_tile_centre makes every staged x_j - cen exact;
+    // decided on the whole tile, so the quarters of a tile agree
+    // sorted: rows in [a, b] = [xs[i0], xs[i0 + T - 1]], columns in [p, q] = [xs[j0], xs[j0 + jtile - 1]]
+    const float a = __ldg(xs + i0), b = __ldg(xs + (i0 + T < n ? i0 + T : n) - 1);
+    const float p = __ldg(xs + j0), q = __ldg(xs + j0 + jtile - 1);
+    const bool wide = psi_tile_wide(a, b, p, q, s);
+    const float cen = (PSI_CENTER && !wide) ? psi_tile_centre(a, q) : 0.f;
     const int64_t jb = j0 + k0;  // first staged column
     // stage the item's column values: float4 loads (xs is 256-byte aligned, jb a multiple of 64)
     if (jcount == kw) {
@@ -123,7 +149,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       // kw / 4 float4: one per thread for kw >= 1024, the first kw / 4 threads otherwise
       for (int q = tid; q < kw / 4; q += kPsiThreads) {
         float4 v = __ldg(src + q);
-        v.x = __fsub_rn(v.x, cen);  // cen = 0 (exact no-op) for the small tiles of R = 0
+        v.x = __fsub_rn(v.x, cen);
         v.y = __fsub_rn(v.y, cen);
         v.z = __fsub_rn(v.z, cen);
         v.w = __fsub_rn(v.w, cen);
@@ -134,39 +160,70 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
     double tt;
-    if constexpr (R == 0) {
-      tt = psi_tile_sum_small<ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
-    } else {
-      if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
-      else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
-    }
+    if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
+    else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
     // next iteration's first __syncthreads orders the smem reuse
   }
-  unsigned long long* g_lo = &ctrl->acc[slot].lo;
-  unsigned long long* g_hi = reinterpret_cast<unsigned long long*>(&ctrl->acc[slot].hi);
-  if (tid == 0 && (cta_acc.lo != 0ull || cta_acc.hi != 0ll)) {
-    unsigned long long old = atomicAdd(g_lo, cta_acc.lo);
-    unsigned long long carry = (old + cta_acc.lo < old) ? 1ull : 0ull;
-    atomicAdd(g_hi, (unsigned long long)cta_acc.hi + carry);
-  }
-  if (fin.what < 0) return;
-  // the last CTA to finish runs the pass's epilogue (threadfence reduction pattern); it also
-  // resets the slot for a later pass on the same workspace
   __shared__ bool last;
-  if (tid == 0) {
-    __threadfence();
-    last = (atomicAdd(&ctrl->psi_done[slot], 1u) == gridDim.x - 1);
+  psi_cta_done(cta_acc, ctrl, slot, fin, n, &last);
+}
+
+// Small tiles (R = 0: n <= kFusedMaxN): one chunk per thread -- a row of a T = 64 tile against the
+// tile's 64 columns (psi_chunk64), the columns read straight from the sorted sample (a few KB:
+// L1-resident) -- the 1024 threads' chunk integers summed per CTA and into the slot.  Work items
+// [tile_begin, tile_end) are tiles, as for psi_kernel; the same chunks and the same integer sums as
+// the single-launch cluster kernel (fused.cu), hence the same bits.
+constexpr int kPsiSmallThreads = 1024;
+
+template <int ORDER>
+__global__ void __launch_bounds__(kPsiSmallThreads, 1)
+psi_small_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
+                 const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, PsiFin fin) {
+  __shared__ Fx128 fxred[kPsiSmallThreads / 32];
+  __shared__ bool last;
+  if (ctrl->grouped) return;  // (never at these sizes: kGroupMinN) as psi_kernel
+  double g = g_host;
+  if (g_dev) {
+    if (*status_dev != PLUGIN_OK) return;
+    g = *g_dev;
   }
-  __syncthreads();
-  if (!last || tid != 0) return;
-  __threadfence();
-  Fx128 total;
-  total.lo = atomicExch(g_lo, 0ull);
-  total.hi = (long long)atomicExch(g_hi, 0ull);
-  ctrl->tile_counter[slot] = 0ull;
-  ctrl->psi_done[slot] = 0u;
-  finalize_total(fin.what, total, atomicAdd(&ctrl->nonfinite, 0) != 0, fin.out, n, fin.g, fin.r, fin.d_psi);
+  const float s = __double2float_rn(1.0 / g);
+  const int64_t nb = (n + kPsiSmallT - 1) / kPsiSmallT;
+  Fx128 acc = {0ull, 0ll};
+  const int64_t c1 = tile_end * kPsiSmallT;
+  for (int64_t c = tile_begin * kPsiSmallT + (int64_t)blockIdx.x * kPsiSmallThreads + threadIdx.x; c < c1;
+       c += (int64_t)gridDim.x * kPsiSmallThreads) {
+    int64_t bi, bj;
+    tile_coords(c / kPsiSmallT, nb, bi, bj);
+    const int64_t i0 = bi * kPsiSmallT, j0 = bj * kPsiSmallT, i = i0 + (c & (kPsiSmallT - 1));
+    if (i >= n) continue;  // padding row
+    // off-diagonal tile whose terms are all exactly zero (psi_kernel's rule; row block bi is full)
+    if (skip && bi != bj && ((double)__ldg(xs + j0) - (double)__ldg(xs + i0 + kPsiSmallT - 1)) * (double)s *
+                                    (1.0 - 1e-5) > kSkipU)
+      continue;
+    const int jcount = (int)((n - j0) < kPsiSmallT ? (n - j0) : kPsiSmallT);
+    fx_add(acc, psi_chunk64<ORDER, true>(xs + j0, jcount, __ldg(xs + i), row_phase(i), dithered_scale(s, i, n),
+                                         row_comp(i), bi == bj ? 1.0 : 2.0));
+  }
+  const Fx128 cta = block_sum_fx<kPsiSmallThreads>(acc, fxred);
+  psi_cta_done(cta, ctrl, slot, fin, n, &last);
+}
+
+template <int ORDER>
+static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, const double* g_dev,
+                                const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tb, int64_t te, cudaStream_t s,
+                                PsiFin fin) {
+  static DevCache cap_cache;
+  const int grid_cap = dev_cached(cap_cache, [](int dev) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_small_kernel<ORDER>, kPsiSmallThreads, 0);
+    return device_sms(dev) * (occ > 0 ? occ : 1);
+  });
+  const int64_t want = ((te - tb) * kPsiSmallT + kPsiSmallThreads - 1) / kPsiSmallThreads;
+  const int grid = (int)(want < grid_cap ? (want < 1 ? 1 : want) : grid_cap);
+  psi_small_kernel<ORDER><<<grid, kPsiSmallThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, fin);
+  return cudaGetLastError();
 }
 
 // resident CTAs of a B200 (148 SMs) at the occupancy the kernel is built for
@@ -265,6 +322,13 @@ cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_hos
     return fin.what >= 0 ? launch_finalize(fin.what, ctrl, slot, nullptr, fin.out, n, fin.g, fin.r, fin.d_psi,
                                            nullptr, s)
                          : cudaSuccess;
+  if (R == 0) {
+#define PLG_SMALL(OO) \
+  if (r == OO) return launch_small<OO>(xs, n, skip, g_host, g_dev, status_dev, ctrl, slot, tile_begin, tile_end, s, fin);
+    PLG_SMALL(6) PLG_SMALL(4) PLG_SMALL(0) PLG_SMALL(2) PLG_SMALL(8) PLG_SMALL(10) PLG_SMALL(12)
+#undef PLG_SMALL
+    return cudaErrorInvalidValue;
+  }
 #define PLG_ORDER(RR, OO)                                                                                  \
   if (r == OO) return launch_t<RR, OO>(xs, n, skip, g_host, g_dev, status_dev, ctrl, slot, tile_begin, tile_end, s, fin);
 #define PLG_CASE(RR)                                                                                       \
@@ -276,7 +340,6 @@ cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_hos
   PLG_CASE(4)
   PLG_CASE(2)
   PLG_CASE(1)
-  PLG_CASE(0)
 #undef PLG_CASE
 #undef PLG_ORDER
   return cudaErrorInvalidValue;

@@ -51,10 +51,12 @@ __device__ __forceinline__ int row_scale_offset(int64_t i, int amp) {
 // s_i = s + k_i ulp(s), exactly (|k_i| << 2^23): symmetric in k_i also when s - |k_i| ulp(s) falls
 // below a power of two (adding k_i to the bit pattern would step by ulp(s)/2 there, a one-sided
 // dilation: measured -1e-5 on psi at s = 1)
-__device__ __forceinline__ float dithered_scale(float s, int64_t i, int64_t n) {
+__device__ __forceinline__ float dither_ulp(float s) {
   const unsigned int e = __float_as_uint(s) & 0x7f800000u;
-  const float ulp = e > (23u << 23) ? __uint_as_float(e - (23u << 23)) : 0.f;  // no dither for s < 2^-103
-  return __fmaf_rn((float)row_scale_offset(i, scale_dither_amp(n)), ulp, s);
+  return e > (23u << 23) ? __uint_as_float(e - (23u << 23)) : 0.f;  // no dither for s < 2^-103
+}
+__device__ __forceinline__ float dithered_scale(float s, int64_t i, int64_t n) {
+  return __fmaf_rn((float)row_scale_offset(i, scale_dither_amp(n)), dither_ulp(s), s);
 }
 
 // He_r(u) for even r as a polynomial in t = u^2 by Horner, monic, exact integer coefficients
@@ -332,57 +334,81 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
 }
 
 // Small tiles for small n (R = 0 in psi_rows_per_thread: n <= kFusedMaxN): T = 64 rows x 64
-// columns, thread tid takes row tid % 64 and the 16 columns 16 (tid / 64) .. + 15, so a pass
-// has 4x more, 16x smaller tiles than at T = 256 and spreads over the SMs (at these sizes the
-// pass is latency-bound).  Same pair arithmetic (pair2, always with the overflow clamp), dither
-// and per-thread fp64 flush; the result is valid in thread 0.  Contains __syncthreads().
+// columns, so a pass has 16x more, 16x smaller tiles than at T = 256 and spreads over the SMs (at
+// these sizes the pass is latency-bound).  The unit of work is a CHUNK: one row of a tile against
+// the tile's 64 columns, with the pair arithmetic of the big tiles' difference-first path (pair2,
+// always with the overflow clamp), the same dither, and one packed fp32 accumulator (even / odd
+// columns) -- the 64-term fp32 chunk of PSI_CH.  Each chunk's value (its fp32 sum in fp64, times
+// the row's 2^(-p_i) and the tile weight) becomes a 128-bit fixed-point integer on its own, so a
+// pass total is the integer sum of its chunks: the same for any assignment of chunks to threads,
+// CTAs or clusters (psi_small_kernel of the multi-kernel path and the single-launch cluster kernel
+// of fused.cu give the same bits).  No barrier.
 constexpr int kPsiSmallT = 64;
 
+__device__ __forceinline__ double row_comp(int64_t i) { return exp2(-(double)row_phase(i)); }
+
+// one chunk from its row's values: v = x_i, p = row_phase(i), si = dithered_scale(s, i, n),
+// comp = row_comp(i); cols: the tile's 64 column values (16-byte aligned; shared or global memory),
+// jcount of them real
 template <int ORDER, bool LDG>
-__device__ __forceinline__ double psi_tile_sum_small(const float* sx, const float* __restrict__ xrows, int64_t n,
-                                                     int64_t i0, int jcount, float s, float xpad, double w,
-                                                     double* red) {
-  const int tid = threadIdx.x;
-  const int64_t i = i0 + (tid & (kPsiSmallT - 1));
-  const int jq = (tid >> 6) * 16;
-  const float v = (i < n) ? (LDG ? __ldg(xrows + i) : xrows[i]) : xpad;
-  const u64 xi = pk2(v, v);
-  const float p = row_phase(i);
-  const u64 ph = pk2(p, p);
-  const float si = dithered_scale(s, i, n);
-  const u64 s2 = pk2(si, si);
-  __syncthreads();
-  const float4* sx4 = reinterpret_cast<const float4*>(sx + jq);
+__device__ __forceinline__ Fx128 psi_chunk64(const float* cols, int jcount, float v, float p, float si, double comp,
+                                             double w) {
+  const u64 xi = pk2(v, v), ph = pk2(p, p), s2 = pk2(si, si);
+  const float4* c4 = reinterpret_cast<const float4*>(cols);
   u64 acc = 0ull;
-  if (jq + 16 <= jcount) {
+  if (jcount >= kPsiSmallT) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 t = sx4[q];
+    for (int q = 0; q < kPsiSmallT / 4; ++q) {
+      const float4 t = LDG ? __ldg(c4 + q) : c4[q];
       pair2<ORDER, false, false, true>(pk2(t.x, t.y), xi, s2, ph, acc);
       pair2<ORDER, false, false, true>(pk2(t.z, t.w), xi, s2, ph, acc);
     }
   } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 t = sx4[q];
-      const int j = jq + 4 * q;
+#pragma unroll 4
+    for (int q = 0; q < kPsiSmallT / 4; ++q) {
+      const int j = 4 * q;
+      float4 t;
+      if (LDG) {  // global memory: no loads past the sample's end
+        t.x = j < jcount ? __ldg(cols + j) : 0.f;
+        t.y = j + 1 < jcount ? __ldg(cols + j + 1) : 0.f;
+        t.z = j + 2 < jcount ? __ldg(cols + j + 2) : 0.f;
+        t.w = j + 3 < jcount ? __ldg(cols + j + 3) : 0.f;
+      } else {
+        t = c4[q];
+      }
       pair2<ORDER, true, false, true>(pk2(t.x, t.y), xi, s2, ph, acc, j < jcount, j + 1 < jcount);
       pair2<ORDER, true, false, true>(pk2(t.z, t.w), xi, s2, ph, acc, j + 2 < jcount, j + 3 < jcount);
     }
   }
   float a0, a1;
   upk2(acc, a0, a1);
-  double tsum = (i < n) ? f32_to_f64_alu(a0 + a1) * exp2(-(double)p) : 0.0;
-  tsum *= w;
-  for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
-  if ((tid & 31) == 0) red[tid >> 5] = tsum;
+  return fx_from_double((double)(a0 + a1) * comp * w);  // F2F: the XU pipe has room at these sizes
+}
+
+// 128-bit fixed-point sums across a warp and a CTA of NT threads (integer: any order, same bits)
+__device__ __forceinline__ Fx128 fx_shfl_xor(Fx128 v, int o) {
+  Fx128 r;
+  r.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+  r.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+  return r;
+}
+__device__ __forceinline__ Fx128 warp_sum_fx(Fx128 v) {
+  for (int o = 16; o; o >>= 1) fx_add(v, fx_shfl_xor(v, o));
+  return v;
+}
+// valid in warp 0; red holds NT / 32 entries; contains __syncthreads() (red may be reused after)
+template <int NT>
+__device__ __forceinline__ Fx128 block_sum_fx(Fx128 v, Fx128* red) {
+  v = warp_sum_fx(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  double tt = 0.0;
-  if (tid == 0) {
-#pragma unroll
-    for (int k = 0; k < kPsiThreads / 32; ++k) tt += red[k];
+  Fx128 t = {0ull, 0ll};
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < NT / 32 ? red[threadIdx.x] : t;
+    t = warp_sum_fx(t);
   }
-  return tt;
+  __syncthreads();
+  return t;
 }
 
 }  // namespace plg

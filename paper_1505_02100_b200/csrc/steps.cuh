@@ -18,20 +18,23 @@ __device__ __forceinline__ double ipow(double b, int k) {
 // w^(-1/k) for finite w > 0, 1 <= k <= 15: a float seed 2^(-log2(w) / k) (MUFU lg2 / ex2 on the
 // mantissa, the exponent split off so the seed cannot leave float range), then three Newton steps
 // z <- z + z (1 - w z^k) / k in fp64 -- no division; quadratic convergence from the ~1e-6 seed
-// to the fp64 fixed point (within a few ulp of the exact root).  A compact rolled loop: the
-// library pow costs ~1 us of latency per call in the single-launch kernel (profiles/r02r_*).
-__device__ __forceinline__ double inv_root(double w, int k) {
+// to the fp64 fixed point (within a few ulp of the exact root).  K is a template parameter so the
+// power by squaring and the steps unroll into one straight dependency chain (the scalar steps sit
+// on the critical path of the single launch); inv_root(w, k) dispatches a runtime k to the same
+// code, so both give the same bits.
+template <int K>
+__device__ __forceinline__ double inv_root_k(double w) {
   int e;
   const double m = frexp(w, &e);  // w = m 2^e, m in [0.5, 1)
-  const double t = -((double)__log2f((float)m) + (double)e) / (double)k;
+  const double t = -((double)__log2f((float)m) + (double)e) / (double)K;
   const double ti = floor(t);
   double z = ldexp((double)exp2f((float)(t - ti)), (int)ti);
-  const double rk = 1.0 / (double)k;
-#pragma unroll 1
+  const double rk = 1.0 / (double)K;
+#pragma unroll
   for (int it = 0; it < 3; ++it) {
-    double zk = 1.0, b = z;  // z^k by squaring
-#pragma unroll 1
-    for (int q = k; q; q >>= 1) {
+    double zk = 1.0, b = z;  // z^K by squaring
+#pragma unroll
+    for (int q = K; q; q >>= 1) {
       if (q & 1) zk *= b;
       b *= b;
     }
@@ -39,15 +42,29 @@ __device__ __forceinline__ double inv_root(double w, int k) {
   }
   return z;
 }
+__device__ __forceinline__ double inv_root(double w, int k) {
+  switch (k) {
+    case 5: return inv_root_k<5>(w);
+    case 7: return inv_root_k<7>(w);
+    case 9: return inv_root_k<9>(w);
+    case 11: return inv_root_k<11>(w);
+    case 13: return inv_root_k<13>(w);
+    default: return inv_root_k<15>(w);  // k = 15: r = 12, the last stage of PLUGIN_DPI_MAX_STAGES
+  }
+}
 
 // the bandwidths of Algorithm 1 and of the l-stage family (Steps III and V):
 // g = (num / (mu2 Psi n))^(1/k) = (mu2 Psi n / num)^(-1/k), num = -2 K^(r)(0), k = r + 3
 __device__ __forceinline__ double plugin_bandwidth(double num, double psi, double nd, int k) {
   return inv_root(kMu2 * psi * nd / num, k);
 }
+template <int K>
+__device__ __forceinline__ double plugin_bandwidth_k(double num, double psi, double nd) {
+  return inv_root_k<K>(kMu2 * psi * nd / num);
+}
 // Step VII: h_z = (R(K) / (mu2^2 Psi4 n))^(1/5)
 __device__ __forceinline__ double plugin_h_z(double psi4_z, double nd) {
-  return inv_root(kMu2 * kMu2 * psi4_z * nd / kRK, 5);
+  return inv_root_k<5>(kMu2 * kMu2 * psi4_z * nd / kRK);
 }
 
 // Step I, one block's share: V is shift invariant, so it is evaluated on
@@ -58,7 +75,8 @@ __device__ __forceinline__ void step1_block(const float* x, int64_t n, double K,
                                             double* sh2, int* sh_bad, double& a, double& q, int& bb) {
   double s1 = 0.0, s2 = 0.0;
   int bad = 0;
-  for (int64_t i = (int64_t)b * 256 + threadIdx.x; i < n; i += (int64_t)nblocks * 256) {
+  // the tree is that of 256 threads; in larger CTAs (fused.cu: 1024) the others add nothing
+  for (int64_t i = (int64_t)b * 256 + threadIdx.x; threadIdx.x < 256 && i < n; i += (int64_t)nblocks * 256) {
     const float v = x[i];
     bad |= !isfinite(v);
     const double d = (double)v - K;
@@ -71,7 +89,7 @@ __device__ __forceinline__ void step1_block(const float* x, int64_t n, double K,
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { sh1[w] = s1; sh2[w] = s2; sh_bad[w] = bad; }
+  if (l == 0 && w < 8) { sh1[w] = s1; sh2[w] = s2; sh_bad[w] = bad; }
   __syncthreads();
   a = 0.0; q = 0.0; bb = 0;
   if (threadIdx.x == 0)
@@ -110,7 +128,7 @@ __device__ __forceinline__ void step1_epilogue(double a, double q, int64_t n, do
   const double psi8_z = 105.0 / (32.0 * sqrt(kPi));
   out->psi8_ns = psi8_z / ipow(sigma, 9);
   // Step III
-  const double g1_z = plugin_bandwidth(-2.0 * kK6at0, psi8_z, nd, 9);
+  const double g1_z = plugin_bandwidth_k<9>(-2.0 * kK6at0, psi8_z, nd);
   out->g1_z = g1_z;
   out->g1 = g1_z * sigma;
 }
@@ -134,7 +152,7 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
     out->psi6 = psi6_z / ipow(sigma, 7);
     if (!(psi6_z < 0.0)) { out->status = PLUGIN_E_DOMAIN; return; }
     // Step V
-    const double g2_z = plugin_bandwidth(-2.0 * kK4at0, psi6_z, nd, 7);
+    const double g2_z = plugin_bandwidth_k<7>(-2.0 * kK4at0, psi6_z, nd);
     out->g2_z = g2_z;
     out->g2 = g2_z * sigma;
   } else {

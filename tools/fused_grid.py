@@ -1,6 +1,6 @@
 """Device time per plugin_h call at small n (the fused single launch), queue kept full: 50
 back-to-back plugin_graph_launch between two events, median of 15 (A/B helper for the grid size,
-PLUGIN_FUSED_GRID).  usage: python tools/fused_grid.py > out.jsonl"""
+PLUGIN_FUSED_CLUSTER).  usage: python tools/fused_grid.py > out.jsonl"""
 import json
 import os
 import statistics
@@ -29,6 +29,6 @@ for n in (128, 256, 512, 1024, 2048):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3 / 50)
-    print(json.dumps({"n": n, "grid_env": os.environ.get("PLUGIN_FUSED_GRID", ""), "us_per_call": statistics.median(ts),
+    print(json.dumps({"n": n, "cluster_env": os.environ.get("PLUGIN_FUSED_CLUSTER", ""), "us_per_call": statistics.median(ts),
                       "h": P.read_result(pg.out)["h"]}), flush=True)
     pg.close()

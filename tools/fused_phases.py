@@ -1,5 +1,5 @@
 """Phase times of the fused single-launch path (a -DPLUGIN_FUSED_TIMING build, loaded through
-PLUGIN_LIB_PATH): sort, Step I-III, each pass, each grid barrier, each finalize, for CTA 0.
+PLUGIN_LIB_PATH): sort (ranks + cluster barrier), Step I-III, each pass, each partial exchange (DSMEM + cluster barrier), each finalize, for CTA 0.
 usage: PLUGIN_LIB_PATH=.../libplugin_ftime.so python tools/fused_phases.py [n ...]"""
 import json
 import os
@@ -14,7 +14,7 @@ import torch  # noqa: E402
 from paper_1505_02100_b200 import inputs  # noqa: E402
 from paper_1505_02100_b200 import plugin as P  # noqa: E402
 
-NAMES = ["sort_step1", "setup", "pass6", "sync6", "final6", "pass4", "sync4", "final4"]
+NAMES = ["load_tables", "slice_keys", "rank_sync_reload", "step1_red", "step1_fin", "pass6", "bsum6", "sync6", "final6", "pass4", "bsum4", "sync4", "final4"]
 
 
 def main():
@@ -30,7 +30,7 @@ def main():
         for it in range(30):
             P.plugin_h(x, ws=ws)
             torch.cuda.synchronize()
-            t = ws[off + 2 * 1024 * 16: off + 2 * 1024 * 16 + 72].clone().view(torch.int64).cpu().tolist()
+            t = ws[off + 2 * 1024 * 16: off + 2 * 1024 * 16 + 8 * (len(NAMES) + 1)].clone().view(torch.int64).cpu().tolist()
             if it >= 5:
                 for i, k in enumerate(NAMES):
                     acc[k].append((t[i + 1] - t[i]) / 1e3)

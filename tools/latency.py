@@ -3,7 +3,7 @@
 Table 2 of the paper times the full algorithm for n = 128..1024 on unpublished
 data; SURVEY §8(d) proposes N(0,1) samples with seeds 100..107 as the stand-in.  Also BASELINE
 configs 1-3.  For each n: device time per call (CUDA events around back-to-back calls on one
-stream, median), for the default path (one cooperative launch when n <= 4096) and the forced
+stream, median), for the default path (one cluster launch when n <= 2048) and the forced
 multi-kernel path, the multi-kernel path replayed from a CUDA graph, and the host-visible time
 of plugin_h_host (H2D of X, the run, D2H of the result, synchronise).
 usage: python tools/latency.py [--reps 200] > gpurun_out/latency.json
@@ -71,7 +71,7 @@ def main():
             P.plugin_h(x, out=out, ws=ws, flags=P.PLUGIN_MULTI_KERNEL)
         med, mn = dev_time(g.replay, a.reps)
         row["graph_multi_kernel_us"], row["graph_multi_kernel_min_us"] = med, mn
-        # the default path (one cooperative launch for n <= 4096) captured in a graph too
+        # the default path (one cluster launch for n <= 2048) captured in a graph too
         try:
             g2 = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g2):
