@@ -75,13 +75,22 @@ __device__ __forceinline__ void step1_block(const float* x, int64_t n, double K,
                                             double* sh2, int* sh_bad, double& a, double& q, int& bb) {
   double s1 = 0.0, s2 = 0.0;
   int bad = 0;
-  // the tree is that of 256 threads; in larger CTAs (fused.cu: 1024) the others add nothing
-  for (int64_t i = (int64_t)b * 256 + threadIdx.x; threadIdx.x < 256 && i < n; i += (int64_t)nblocks * 256) {
-    const float v = x[i];
-    bad |= !isfinite(v);
-    const double d = (double)v - K;
-    s1 += d;
-    s2 = fma(d, d, s2);
+  // the tree is that of 256 threads; in larger CTAs (fused.cu: 1024) the others add nothing.  Up to
+  // 8 values are loaded before they are added (independent loads in flight; the same additions in
+  // the same order)
+  const int64_t stride = (int64_t)nblocks * 256;
+  for (int64_t i0 = (int64_t)b * 256 + threadIdx.x; threadIdx.x < 256 && i0 < n; i0 += 8 * stride) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (i0 + k * stride < n) ? x[i0 + k * stride] : 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i0 + k * stride >= n) break;
+      bad |= !isfinite(v[k]);
+      const double d = (double)v[k] - K;
+      s1 += d;
+      s2 = fma(d, d, s2);
+    }
   }
   for (int o = 16; o; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
