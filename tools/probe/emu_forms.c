@@ -11,6 +11,8 @@
 // form:  0 t-form (round 1: u, t = u u, a = t c + p, P(t), acc)
 //        1 a-form (v = u sqrt(log2 e / 2), a = p - v v, Q(a) monic with per-row coefficients)
 //        2 a-form with the row offset's low part folded in (a = fma(-v, v, p) - 2 v X_lo)
+//        3 depressed polynomial (t' = fma(u, u, -k), k = 5 for r = 6, 3 for r = 4; a = fma(t', c, p + k c);
+//          P6 = t'(t'^2 - 30) - 40, P4 = t'^2 - 6: one FP32 op fewer per pair)
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -123,7 +125,28 @@ int main(int argc, char** argv) {
         }
         const float xi_c = x[i] - cen;
         float acc0 = 0.f, acc1 = 0.f;
-        if (form == 0) {
+        if (form == 3) {  // depressed polynomial: t' = fma(u, u, -k), a = fma(t', c, p'), P(t')
+          const float ulps = u2f((f2u(sf) & 0x7f800000u) - (23u << 23));
+          const float si = fmaf((float)k, ulps, sf);
+          const float Xi = -(xi_c * si);
+          const float kk = (r == 6) ? 5.f : 3.f;
+          const float php = p + kk * c2f;  // fp32 (one rounding); the undo uses it exactly
+          const double compp = exp2(-((double)php - (double)kk * (double)c2f));
+          for (int64_t j = rj0; j < jend; ++j) {
+            const float xj_c = x[j] - cen;
+            const float u = fmaf(xj_c, si, Xi);
+            const float tp = fmaf(u, u, -kk);
+            const float a = fmaf(tp, c2f, php);
+            const float e = (float)exp2((double)a);
+            const float P = (r == 6) ? fmaf(tp, fmaf(tp, tp, -30.f), -40.f) : fmaf(tp, tp, -6.f);
+            float* ac = ((j - rj0) & 1) ? &acc1 : &acc0;
+            *ac = fmaf(P, e, *ac);
+            if (((j - rj0) & 63) == 63 || j == jend - 1) {
+              rgpu += (double)(acc0 + acc1) * compp;
+              acc0 = acc1 = 0.f;
+            }
+          }
+        } else if (form == 0) {
           const float ulps = u2f((f2u(sf) & 0x7f800000u) - (23u << 23));
           const float si = fmaf((float)k, ulps, sf);  // s + k ulp(s), exact and symmetric in k
           const float Xi = -(xi_c * si);
