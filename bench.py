@@ -671,10 +671,13 @@ def run_batch(a):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_meas = clocks.get("sm_mhz") or 1965.0
     peak = MUFU_EX2_PER_CLK_PER_SM * sms * f_meas * 1e6 / 1e9
-    # the batch kernel's tiles (T = 256 R; diagonal tiles as full squares): nb (nb + 1) / 2 of T^2
-    T = 256 * int(os.environ.get("PLUGIN_BATCH_R_REPORT", "1"))
+    # the batch kernel's tiles (T = 256, n a multiple of T here): nb (nb - 1) / 2 off-diagonal tiles
+    # of T^2 pairs; each diagonal tile evaluates its 64-wide diagonal squares in both orders and the
+    # 64-column chunks right of them once (psi_tile_sum<..., DIAG>): 64^2 B (B + 1) / 2, B = T / 64
+    T = 256
     nbt = -(-n // T)
-    evaluated = count * 2 * (nbt * (nbt + 1) // 2) * min(T, n) ** 2
+    B = T // 64
+    evaluated = count * 2 * (nbt * (nbt - 1) // 2 * T * T + nbt * 64 * 64 * B * (B + 1) // 2)
     res = P.read_results(out, 2)
     line = {"metric": "pairwise K4/K6 evaluations/sec, batches of independent samples", "value": pairs / (ms / 1e3) / 1e9,
             "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,

@@ -296,8 +296,9 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
 // b (2 <= n_b <= 2048) on its own -- no grid barrier: the prologue above (the same sort and
 // Step I as plugin_h), then each pass over tiles of T = 256 BATCH_R (the centred form of psi.cu;
 // at one CTA per sample the T = 64 tiles of the latency path are overhead-bound, and larger
-// tiles waste more on the full-square diagonal tiles: T = 256 measured fastest) and the same
-// finalize.  The tiles differ
+// tiles waste more on the diagonal tiles: T = 256 measured fastest; diagonal tiles evaluate only
+// their 64-wide diagonal squares and the chunks right of them, psi_tile_sum<..., DIAG>) and the
+// same finalize.  The tiles differ
 // from plugin_h's, so results agree with it to fp32 evaluation rounding, not bit for bit.
 #ifndef BATCH_R
 #define BATCH_R 1  // rows per thread of the batch tiles (T = 256 R); A/B: 1 fastest (less full-square waste)
@@ -358,8 +359,10 @@ plugin_batch_kernel(const float* __restrict__ x, const int64_t* __restrict__ off
         if (wide)  // see psi_tile_wide; out of line so the common path keeps its code and registers
           tt = batch_wide_tile(pass, sx, xsm, n, i0, jcount, s, xpad, w, red);
         else
-          tt = (pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
-                           : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen);
+          tt = (PSI_DIAG_BAND && bi == bj) ? ((pass == 0) ? psi_tile_sum<kBatchR, 6, false, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
+                                         : psi_tile_sum<kBatchR, 4, false, false, true>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen))
+                          : ((pass == 0) ? psi_tile_sum<kBatchR, 6, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen)
+                                         : psi_tile_sum<kBatchR, 4, false>(sx, xsm, n, i0, jcount, s, xpad, w, red, cen));
         if (tid == 0) fx_add(acc, fx_from_double(tt));
       }
       if (tid == 0) finalize_pass(pass, fx_to_double(acc), n, &res);

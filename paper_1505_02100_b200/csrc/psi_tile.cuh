@@ -236,10 +236,19 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
 // cen: the tile centre when PSI_CENTER (sx then holds fl(x_j - cen)); ignored otherwise
 // WIDE (psi_tile_wide): difference first (sx holds raw values, cen unused) and pair2's overflow
 // clamp; the inner loop stays rolled there to keep the code small.
-template <int R, int ORDER, bool LDG, bool WIDE = false>
+// DIAG (R = 1, a diagonal tile, w = 1): row t starts at its own 64-column band b = t / 64 -- the
+// band's 64 x 64 diagonal square is evaluated in both orders (weight 1) and the chunks right of it
+// once with weight 2 (the mirror image below the diagonal is skipped: K is even); the lanes of a warp
+// share b, so the column loop stays uniform.  10 of 16 chunk units of a T = 256 diagonal tile
+// instead of 16.
+#ifndef PSI_DIAG_BAND
+#define PSI_DIAG_BAND 1  // 0: diagonal tiles as full squares (A/B only)
+#endif
+template <int R, int ORDER, bool LDG, bool WIDE = false, bool DIAG = false>
 __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __restrict__ xrows, int64_t n, int64_t i0,
                                                int jcount, float s, float xpad, double w, double* red,
                                                float cen = 0.f) {
+  static_assert(!DIAG || (R == 1 && PSI_CH == 64), "diagonal banding: one row per thread, 64-column chunks");
   constexpr int CH = PSI_CH;  // j per fp32 chunk (CH/2 per packed lane) before the fp64 flush
   constexpr bool CEN = PSI_CENTER != 0 && !WIDE;
   constexpr bool CLAMP = WIDE;
@@ -261,7 +270,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
   __syncthreads();
   const float4* sx4 = reinterpret_cast<const float4*>(sx);
   const int full = jcount / CH;
-  for (int c = 0; c < full; ++c) {
+  const int band = DIAG ? (tid >> 6) : 0;  // the row's diagonal chunk (DIAG)
+  for (int c = band; c < full; ++c) {
     u64 acc[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0ull;
@@ -288,10 +298,11 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
     for (int k = 0; k < R; ++k) {
       float a0, a1;
       upk2(acc[k], a0, a1);
-      drow[k] += f32_to_f64_alu(a0 + a1);
+      const double v = f32_to_f64_alu(a0 + a1);
+      drow[k] += (DIAG && c > band) ? 2.0 * v : v;
     }
   }
-  if (full * CH < jcount) {  // ragged last chunk of the last column tile
+  if (full * CH < jcount && full >= band) {  // ragged last chunk of the last column tile
     u64 acc[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0ull;
@@ -310,7 +321,8 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
     for (int k = 0; k < R; ++k) {
       float a0, a1;
       upk2(acc[k], a0, a1);
-      drow[k] += f32_to_f64_alu(a0 + a1);
+      const double v = f32_to_f64_alu(a0 + a1);
+      drow[k] += (DIAG && full > band) ? 2.0 * v : v;
     }
   }
   // undo the dither per row, drop padding rows, weight the tile
