@@ -106,6 +106,7 @@ constexpr int kFusedSliceMax = (int)(kFusedMaxN / 8) + 4;  // slice length at th
 // merged by binary search (two exchanges, O(n log n)); measured: the counting sort takes 1.4 / 3.6 us
 // at n = 128 / 1024 against 3.0 / 4.0 for the merge, 10.2 against 5.0 at n = 2048
 constexpr int64_t kFusedCountMaxN = 1024;
+static_assert(kFusedCountMaxN <= kFusedThreads, "one key per thread in the counting sort");
 __host__ __device__ inline int fused_nsx(int64_t n) { return (int)((n + kPsiSmallT - 1) / kPsiSmallT * kPsiSmallT); }
 __host__ __device__ inline int fused_tiles(int64_t n) { const int nb = fused_nsx(n) / kPsiSmallT; return nb * (nb + 1) / 2; }
 __host__ __device__ inline int fused_runs(int64_t n) { return (int)n + 5 * kFusedClusterMax; }
@@ -149,14 +150,13 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
   while (mp < m) mp <<= 1;
   int lp = 5;  // P = min(32, 1024 / mp) lanes per key
   while (lp > 0 && (mp << lp) > kFusedThreads) --lp;
+  // counting (n <= 1024 = threads): all n composites in runs[], the slice a part of them; else the
+  // slice's m composites in sk[].  The load is issued first and stored after the tables below, so
+  // its latency overlaps their arithmetic.
   const bool counting = n <= kFusedCountMaxN;
-  if (counting) {  // all n composites (runs[] holds them); the slice is a part of them
-    for (int i = tid; i < (int)n; i += kFusedThreads)
-      runs[i] = ((unsigned long long)blocksort_key(__ldg(xb + i)) << 32) | (unsigned int)i;
-  } else {
-    for (int k = tid; k < m; k += kFusedThreads)
-      sk[k] = k < mm ? ((unsigned long long)blocksort_key(__ldg(xb + lo + k)) << 32) | (unsigned int)(lo + k) : ~0ull;
-  }
+  const int kidx = counting ? tid : lo + tid;
+  const bool kreal = counting ? tid < (int)n : tid < mm;
+  const unsigned int kraw = kreal ? __ldg(xb + kidx) : 0u;
   if (tid == 0) init_result(&res, n);
   // pass-independent row tables and the tile table (tile t -> block row, block column)
   const int64_t nb = nsx / kPsiSmallT, tiles = nb * (nb + 1) / 2;
@@ -169,6 +169,14 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
     int64_t bi, bj;
     tile_coords(t, nb, bi, bj);
     ttab[t] = (unsigned short)((bi << 8) | bj);
+  }
+  {
+    const unsigned long long comp64 = ((unsigned long long)blocksort_key(kraw) << 32) | (unsigned int)kidx;
+    if (counting) {
+      if (kreal) runs[tid] = comp64;
+    } else if (tid < m) {
+      sk[tid] = kreal ? comp64 : ~0ull;
+    }
   }
   __syncthreads();
   FT_MARK(1);
