@@ -294,7 +294,7 @@ def _same(a, b):
 
 @pytest.mark.parametrize("n", [2, 3, 31, 63, 64, 65, 255, 256, 257, 1000, 1024, 1025, 2047, 2048, 2049, 4096])
 def test_fused_small_n_bit_identical_to_multi_kernel(P, oracle_mod, n):
-    # n <= 2048: plugin_h runs one cooperative launch (fused.cu); it must reproduce the
+    # n <= 2048: plugin_h runs one thread-block-cluster launch (fused.cu); it must reproduce the
     # multi-kernel sequence bit for bit, and both must match the oracle
     x = inputs.mixture(n, 300 + n) if n > 3 else inputs.normal(n, 300 + n)
     xt = torch.from_numpy(x).cuda()
@@ -306,6 +306,35 @@ def test_fused_small_n_bit_identical_to_multi_kernel(P, oracle_mod, n):
     o = oracle_mod.plugin(x)
     for key in ("psi6_z", "psi4_z", "h", "g1", "g2", "sigma"):
         assert rel(a[key], o[key]) < TOL, (n, key, a[key], o[key])
+
+
+def test_fused_cluster_of_8_bit_identical(P):
+    # the single launch falls back to an 8-CTA cluster where 16 cannot be scheduled
+    # (PLUGIN_FUSED_CLUSTER=8 forces it; read once per process, hence the subprocess): other
+    # slices, other chunk-to-CTA deals, the same bits (integer chunk sums)
+    import subprocess
+    import sys
+    sizes = [2, 65, 700, 1024, 1025, 1500, 2048]
+    code = (
+        "import json, sys, torch\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_1505_02100_b200 import inputs, plugin as P\n"
+        "out = {}\n"
+        "for n in %r:\n"
+        "    x = inputs.mixture(n, 900 + n) if n > 3 else inputs.normal(n, 900 + n)\n"
+        "    r = P.read_result(P.plugin_h(torch.from_numpy(x).cuda()))\n"
+        "    out[n] = {k: float(r[k]).hex() for k in ('psi6', 'psi4', 'h', 'g1', 'g2', 'sigma')}\n"
+        "print(json.dumps(out))\n" % (os.path.dirname(HERE), sizes))
+    env = dict(os.environ, PLUGIN_FUSED_CLUSTER="8")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    for n in sizes:
+        x = inputs.mixture(n, 900 + n) if n > 3 else inputs.normal(n, 900 + n)
+        r = P.read_result(P.plugin_h(torch.from_numpy(x).cuda()))
+        mk = P.read_result(P.plugin_h(torch.from_numpy(x).cuda(), flags=P.PLUGIN_MULTI_KERNEL))
+        for k, v in got[str(n)].items():
+            assert float.fromhex(v) == r[k] == mk[k], (n, k, v, r[k], mk[k])
 
 
 @pytest.mark.parametrize("case", ["constant", "nan", "inf"])
