@@ -106,6 +106,11 @@ constexpr int kFusedSliceMax = (int)(kFusedMaxN / 8) + 4;  // slice length at th
 // merged by binary search (two exchanges, O(n log n)); measured: the counting sort takes 1.4 / 3.6 us
 // at n = 128 / 1024 against 3.0 / 4.0 for the merge, 10.2 against 5.0 at n = 2048
 constexpr int64_t kFusedCountMaxN = 1024;
+// up to this n every CTA ranks all n keys itself and writes its own copy of the ascending array:
+// no exchange and no cluster barrier in the sort (n^2 / 1024 compares per thread); measured: the
+// local sort takes 0.9 us at n = 128 (against 1.8 us with the exchange: 14.4 -> 12.4 us per call)
+// and 2.5 us at n = 256 (against 1.4 us)
+constexpr int64_t kFusedLocalSortN = 160;
 static_assert(kFusedCountMaxN <= kFusedThreads, "one key per thread in the counting sort");
 __host__ __device__ inline int fused_nsx(int64_t n) { return (int)((n + kPsiSmallT - 1) / kPsiSmallT * kPsiSmallT); }
 __host__ __device__ inline int fused_tiles(int64_t n) { const int nb = fused_nsx(n) / kPsiSmallT; return nb * (nb + 1) / 2; }
@@ -133,6 +138,11 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
+  const bool local_sort = n <= kFusedLocalSortN;
+  // before a CTA writes into another's shared memory, every CTA of the cluster must be running: the
+  // sort's cluster barriers see to it, and with the local sort an arrive here and a wait before the
+  // first exchange do
+  if (local_sort) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   FT_MARK(0);
 
   // ---- sort: C sorted slices, merged by rank ----
@@ -183,55 +193,72 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
   unsigned long long* grun = reinterpret_cast<unsigned long long*>(parts);            // C runs of m
   float* srt = reinterpret_cast<float*>(grun + kFusedMaxN + 4 * kFusedClusterMax);  // the ascending array
   const int ks = tid >> lp, part = tid & ((1 << lp) - 1);
-  if (counting) {
-    // small n: every CTA holds all n composites and counts those below each of its keys (P lanes
-    // per key, over the composites q = part (mod P))
-    const unsigned long long* key = runs;
-    FT_MARK(2);
+  if (local_sort) {
+    // every CTA: all n keys, P = 2^lq lanes per key, straight into its own sample
+    int lq = 5;
+    while (lq > 0 && ((int)n << lq) > kFusedThreads) --lq;
+    const int kk = tid >> lq, pp = tid & ((1 << lq) - 1);
     unsigned int cnt = 0;
-    const unsigned long long ki = ks < mm ? key[lo + ks] : ~0ull;
-    if (ks < mm) {
+    const unsigned long long ki = kk < n ? runs[kk] : ~0ull;
+    if (kk < n) {
 #pragma unroll 4
-      for (int q = part; q < (int)n; q += 1 << lp) cnt += key[q] < ki;
+      for (int q = pp; q < (int)n; q += 1 << lq) cnt += runs[q] < ki;
     }
-    for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
-  } else {
-    const bool own = ks < m;
-    const unsigned long long ki = own ? sk[ks] : ~0ull;
-    {
-      unsigned int cnt = 0;
-      for (int q = part; q < m; q += 1 << lp) cnt += sk[q] < ki;
-      for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      // pads (~0, all equal) keep their slots after the mm real keys
-      if (own && part == 0) grun[lo + (ks < mm ? (int)cnt : ks)] = ki;
-    }
-    cluster.sync();  // release / acquire at cluster scope: every run is in the workspace
-    // runs at a stride of m + 1 composites in shared memory: the P lanes of a key search P different
-    // runs in lockstep, and an even stride would put them all on the same banks
-    for (int e = tid; e < C * m; e += kFusedThreads) {
-      const int r = e / m;
-      runs[e + r] = __ldcg(grun + e);
-    }
-    __syncthreads();
+    for (int o = 1; o < (1 << lq); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     FT_MARK(2);
-    unsigned int cnt = 0;
-    if (ks < mm) {
-      for (int r = part; r < C; r += 1 << lp) {  // composites below ki in run r (pads never count)
-        const unsigned long long* run = runs + r * (m + 1);
-        int pos = 0;
-        for (int step = mp; step >= 1; step >>= 1)
-          if (pos + step <= m && run[pos + step - 1] < ki) pos += step;
-        cnt += (unsigned int)pos;
+    if (kk < n && pp == 0) xsm[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
+    __syncthreads();
+  } else {
+    if (counting) {
+      // small n: every CTA holds all n composites and counts those below each of its keys (P lanes
+      // per key, over the composites q = part (mod P))
+      const unsigned long long* key = runs;
+      FT_MARK(2);
+      unsigned int cnt = 0;
+      const unsigned long long ki = ks < mm ? key[lo + ks] : ~0ull;
+      if (ks < mm) {
+  #pragma unroll 4
+        for (int q = part; q < (int)n; q += 1 << lp) cnt += key[q] < ki;
       }
+      for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
+    } else {
+      const bool own = ks < m;
+      const unsigned long long ki = own ? sk[ks] : ~0ull;
+      {
+        unsigned int cnt = 0;
+        for (int q = part; q < m; q += 1 << lp) cnt += sk[q] < ki;
+        for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        // pads (~0, all equal) keep their slots after the mm real keys
+        if (own && part == 0) grun[lo + (ks < mm ? (int)cnt : ks)] = ki;
+      }
+      cluster.sync();  // release / acquire at cluster scope: every run is in the workspace
+      // runs at a stride of m + 1 composites in shared memory: the P lanes of a key search P different
+      // runs in lockstep, and an even stride would put them all on the same banks
+      for (int e = tid; e < C * m; e += kFusedThreads) {
+        const int r = e / m;
+        runs[e + r] = __ldcg(grun + e);
+      }
+      __syncthreads();
+      FT_MARK(2);
+      unsigned int cnt = 0;
+      if (ks < mm) {
+        for (int r = part; r < C; r += 1 << lp) {  // composites below ki in run r (pads never count)
+          const unsigned long long* run = runs + r * (m + 1);
+          int pos = 0;
+          for (int step = mp; step >= 1; step >>= 1)
+            if (pos + step <= m && run[pos + step - 1] < ki) pos += step;
+          cnt += (unsigned int)pos;
+        }
+      }
+      for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
     }
-    for (int o = 1; o < (1 << lp); o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (ks < mm && part == 0) srt[cnt] = __uint_as_float(key2bits((unsigned int)(ki >> 32)));
+    cluster.sync();  // every value is at its rank
+    for (int q = tid; q < n4; q += kFusedThreads)
+      reinterpret_cast<float4*>(xsm)[q] = __ldcg(reinterpret_cast<const float4*>(srt) + q);
+    __syncthreads();
   }
-  cluster.sync();  // every value is at its rank
-  for (int q = tid; q < n4; q += kFusedThreads)
-    reinterpret_cast<float4*>(xsm)[q] = __ldcg(reinterpret_cast<const float4*>(srt) + q);
-  __syncthreads();
   FT_MARK(3);
 
   // ---- Steps I-III ----
@@ -284,6 +311,7 @@ plugin_cluster_kernel(const float* __restrict__ x, int64_t n, int skip, plugin_r
     FT_MARK(6 + 4 * pass);
     const Fx128 cta = block_sum_fx<kFusedThreads>(acc, fxred);  // valid in warp 0
     FT_MARK(7 + 4 * pass);
+    if (pass == 0 && local_sort) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     // pass 6: to every CTA (each finalises Step V); pass 4: to CTA 0
     if (tid < (pass == 0 ? C : 1)) cluster.map_shared_rank(&cparts[pass][0], tid)[crank] = cta;
     cluster.sync();
