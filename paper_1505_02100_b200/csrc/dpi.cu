@@ -79,7 +79,7 @@ __global__ void dpi_finalize_kernel(Ctrl* ctrl, int slot, int j, plugin_dpi_resu
   const double nd = (double)out->n;
   const double S = fx_to_double(acc);  // sum_i sum_j K^(r)(u_ij) / phi(0)
   const double g_z = out->g_z[j - 1];
-  const double psi_z = kInvSqrt2Pi * S / (nd * nd * ipow(g_z, r + 1));
+  const double psi_z = psi_z_from_sum(S, nd, g_z, r);
   out->psi_z[j - 1] = psi_z;
   out->psi[j - 1] = psi_z / ipow(out->sigma, r + 1);
   if (j > 1) dpi_bandwidth(out, j - 1, psi_z, nd);

@@ -26,7 +26,8 @@ template <int K>
 __device__ __forceinline__ double inv_root_k(double w) {
   int e;
   const double m = frexp(w, &e);  // w = m 2^e, m in [0.5, 1)
-  const double t = -((double)__log2f((float)m) + (double)e) / (double)K;
+  constexpr double kNegInvK = -1.0 / (double)K;
+  const double t = ((double)__log2f((float)m) + (double)e) * kNegInvK;
   const double ti = floor(t);
   double z = ldexp((double)exp2f((float)(t - ti)), (int)ti);
   const double rk = 1.0 / (double)K;
@@ -55,16 +56,17 @@ __device__ __forceinline__ double inv_root(double w, int k) {
 
 // the bandwidths of Algorithm 1 and of the l-stage family (Steps III and V):
 // g = (num / (mu2 Psi n))^(1/k) = (mu2 Psi n / num)^(-1/k), num = -2 K^(r)(0), k = r + 3
+// (the data-independent factor mu2 n / num first: one multiply after psi on the critical path)
 __device__ __forceinline__ double plugin_bandwidth(double num, double psi, double nd, int k) {
-  return inv_root(kMu2 * psi * nd / num, k);
+  return inv_root(psi * (kMu2 * nd / num), k);
 }
 template <int K>
 __device__ __forceinline__ double plugin_bandwidth_k(double num, double psi, double nd) {
-  return inv_root_k<K>(kMu2 * psi * nd / num);
+  return inv_root_k<K>(psi * (kMu2 * nd / num));
 }
 // Step VII: h_z = (R(K) / (mu2^2 Psi4 n))^(1/5)
 __device__ __forceinline__ double plugin_h_z(double psi4_z, double nd) {
-  return inv_root_k<5>(kMu2 * kMu2 * psi4_z * nd / kRK);
+  return inv_root_k<5>(psi4_z * (kMu2 * kMu2 * nd / kRK));
 }
 
 // Step I, one block's share: V is shift invariant, so it is evaluated on
@@ -126,8 +128,9 @@ __device__ __forceinline__ void step1_total(const double* partials, int nblocks,
 __device__ __forceinline__ void step1_epilogue(double a, double q, int64_t n, double K, bool nonfinite,
                                                plugin_result* out) {
   const double nd = (double)n;
-  const double var = (q - a * a / nd) / (nd - 1.0);
-  out->mean = K + a / nd;
+  const double rn = 1.0 / nd, rn1 = 1.0 / (nd - 1.0);  // data-independent: off the critical path
+  const double var = (q - a * a * rn) * rn1;
+  out->mean = K + a * rn;
   out->var = var;
   if (nonfinite) { out->status = PLUGIN_E_NONFINITE; return; }
   if (!(var > 0.0)) { out->status = PLUGIN_E_DEGENERATE; return; }
@@ -140,6 +143,13 @@ __device__ __forceinline__ void step1_epilogue(double a, double q, int64_t n, do
   const double g1_z = plugin_bandwidth_k<9>(-2.0 * kK6at0, psi8_z, nd);
   out->g1_z = g1_z;
   out->g1 = g1_z * sigma;
+}
+
+// Psi_r in z units from the pass sum S = sum_i sum_j K^(r)(u_ij) / phi(0) (Eq. 6/7 with the
+// symmetry): phi(0) S / (n^2 g_z^(r+1)), the data-independent factor formed first (one multiply
+// after S on the critical path); finalize_pass and the DPI stages share it (bit-identical l = 2)
+__device__ __forceinline__ double psi_z_from_sum(double S, double nd, double g_z, int r) {
+  return S * (kInvSqrt2Pi / (nd * nd * ipow(g_z, r + 1)));
 }
 
 __device__ __forceinline__ double fx_to_double(Fx128 v) {
@@ -155,7 +165,7 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
   if (what == 0) {
     // Step IV (Eq. 6) in z units: u = (z_i - z_j)/g1_z = (X_i - X_j)/g1
     const double g1_z = out->g1_z;
-    const double psi6_z = kInvSqrt2Pi * S / (nd * nd * ipow(g1_z, 7));
+    const double psi6_z = psi_z_from_sum(S, nd, g1_z, 6);
     out->S6 = S;
     out->psi6_z = psi6_z;
     out->psi6 = psi6_z / ipow(sigma, 7);
@@ -167,7 +177,7 @@ __device__ __forceinline__ void finalize_pass(int what, double S, int64_t n, plu
   } else {
     // Step VI (Eq. 7)
     const double g2_z = out->g2_z;
-    const double psi4_z = kInvSqrt2Pi * S / (nd * nd * ipow(g2_z, 5));
+    const double psi4_z = psi_z_from_sum(S, nd, g2_z, 4);
     out->S4 = S;
     out->psi4_z = psi4_z;
     out->psi4 = psi4_z / ipow(sigma, 5);
