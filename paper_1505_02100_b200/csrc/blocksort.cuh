@@ -15,6 +15,11 @@
 
 namespace plg {
 
+// phase marks of the block sort (sort.cu defines SB_MARK under -DSORT_TIMING; empty elsewhere)
+#ifndef SB_MARK
+#define SB_MARK(k) do { } while (0)
+#endif
+
 constexpr int kBlockSortN = 2048;  // keys per CTA (256 threads x 8)
 
 __device__ __forceinline__ void cmpx(unsigned int& a, unsigned int& b, bool asc) {
@@ -67,12 +72,15 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
   int lgmax = 8;  // runs of 2^lgmax cover the cnt keys
   while ((1 << lgmax) < cnt) ++lgmax;
   const int active = 1 << lgmax;  // positions that take part (the rest are pads)
+  SB_MARK(1);
   if ((w << 8) < active) warp_sort256(k);  // runs of pads only are sorted already
+  SB_MARK(2);
   unsigned int* src = (lgmax - 8) & 1 ? a : out;  // the last round writes out
   unsigned int* dst = (lgmax - 8) & 1 ? out : a;
 #pragma unroll
   for (int r = 0; r < 8; ++r) src[(w << 8) + (lane << 3) + r] = k[r];
   __syncthreads();
+  SB_MARK(3);
 #pragma unroll 1
   for (int lg = 8; lg < lgmax; ++lg) {  // runs of L = 2^lg merged pairwise (merge path)
     const int L = 1 << lg;
@@ -99,6 +107,7 @@ __device__ __forceinline__ void cta_sort2048(unsigned int (&k)[8], unsigned int*
       }
     }
     __syncthreads();
+    SB_MARK(lg - 4);  // 4, 5, 6 after the rounds of runs 256, 512, 1024
     unsigned int* tmp = src;
     src = dst;
     dst = tmp;

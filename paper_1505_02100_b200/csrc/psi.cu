@@ -37,6 +37,23 @@
 
 namespace plg {
 
+// -DPSI_TIMING (tools/psi_phases.py, never in the product build): thread 0 of each CTA records
+// %globaltimer (ns) at the phase boundaries of its first tile, its SM and its tile count into
+// g_psi_timing (8 words per CTA; plugin_debug_psi_timing copies them out)
+#ifdef PSI_TIMING
+constexpr int kPsiTimingCtas = 4096;
+__device__ unsigned long long g_psi_timing[kPsiTimingCtas * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PT_MARK(k, v) \
+  do { if (threadIdx.x == 0 && blockIdx.x < kPsiTimingCtas) g_psi_timing[blockIdx.x * 8 + (k)] = (v); } while (0)
+#else
+#define PT_MARK(k, v) do { } while (0)
+#endif
+
 // a pass CTA's exact partial into the slot; with a PsiFin, the last CTA to finish runs the pass's
 // epilogue (threadfence reduction pattern) and resets the slot for a later pass on the same
 // workspace.  cta_acc valid in thread 0; called by every thread; last: a shared flag.
@@ -98,11 +115,23 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   const float xpad = __ldg(xs + n - 1);
   Fx128 cta_acc = {0ull, 0ll};
   const int tid = threadIdx.x;
+#ifdef PSI_TIMING
+  int ntiles = 0;
+  PT_MARK(0, gtimer());
+  {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    PT_MARK(6, smid);
+  }
+#endif
 
   for (;;) {
     if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
     __syncthreads();
     const int64_t item = s_tile;
+#ifdef PSI_TIMING
+    if (ntiles == 0) PT_MARK(1, gtimer());
+#endif
     if (item >= tile_end) break;
     // work item -> tile t and its column range [k0, k0 + kw): items < head are whole tiles, the
     // rest are column quarters of the tail tiles (psi_tail_head)
@@ -159,14 +188,28 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
       for (int q = tid; q < kw; q += kPsiThreads) sx[q] = __fsub_rn((q < jcount) ? __ldg(xs + jb + q) : xpad, cen);
     }
     const double w = (bi == bj) ? 1.0 : 2.0;
+#ifdef PSI_TIMING
+    if (ntiles == 0) PT_MARK(2, gtimer());
+#endif
     double tt;
     if (wide) tt = psi_tile_sum<R, ORDER, true, true>(sx, xs, n, i0, jcount, s, xpad, w, red);
     else tt = psi_tile_sum<R, ORDER, true>(sx, xs, n, i0, jcount, s, xpad, w, red, cen);
     if (tid == 0) fx_add(cta_acc, fx_from_double(tt));
+#ifdef PSI_TIMING
+    if (ntiles == 0) PT_MARK(3, gtimer());
+    ++ntiles;
+#endif
     // next iteration's first __syncthreads orders the smem reuse
   }
   __shared__ bool last;
+#ifdef PSI_TIMING
+  PT_MARK(4, gtimer());
+  PT_MARK(7, ntiles);
+#endif
   psi_cta_done(cta_acc, ctrl, slot, fin, n, &last);
+#ifdef PSI_TIMING
+  PT_MARK(5, gtimer());
+#endif
 }
 
 // Small tiles (R = 0: n <= kFusedMaxN): one chunk per thread -- a row of a T = 64 tile against the
@@ -346,3 +389,10 @@ cudaError_t launch_psi(const float* xs, int64_t n, int r, int skip, double g_hos
 }
 
 }  // namespace plg
+
+#ifdef PSI_TIMING
+extern "C" int plugin_debug_psi_timing(void* host, int ctas) {
+  if (ctas > plg::kPsiTimingCtas) ctas = plg::kPsiTimingCtas;
+  return (int)cudaMemcpyFromSymbol(host, plg::g_psi_timing, sizeof(unsigned long long) * 8 * (size_t)ctas);
+}
+#endif

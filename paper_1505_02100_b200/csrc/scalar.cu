@@ -8,6 +8,22 @@
 
 namespace plg {
 
+// -DSORT_TIMING: step1_kernel's marks (entry, block sums done, counter taken, epilogue done) in
+// g_step1_timing (4 words per CTA, tools/sort_phases.py)
+#ifdef SORT_TIMING
+__device__ unsigned long long g_step1_timing[64 * 4];
+#define S1_MARK(k)                                                             \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 64) {                                 \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      g_step1_timing[blockIdx.x * 4 + (k)] = t_;                               \
+    }                                                                          \
+  } while (0)
+#else
+#define S1_MARK(k) do { } while (0)
+#endif
+
 // Step I over a fixed grid (bit-reproducible; see steps.cuh), with the result record's
 // initialisation and the Steps II-III epilogue in the last block to finish.
 __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x, int64_t n, Ctrl* ctrl,
@@ -15,10 +31,12 @@ __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x,
   __shared__ double sh1[8], sh2[8];
   __shared__ int sh_bad[8];
   __shared__ bool last;
+  S1_MARK(0);
   const double K = (double)x[0];
   double a, q;
   int bb;
   step1_block(x, n, K, blockIdx.x, gridDim.x, sh1, sh2, sh_bad, a, q, bb);
+  S1_MARK(1);
   if (threadIdx.x == 0) {
     partials[2 * blockIdx.x] = a;
     partials[2 * blockIdx.x + 1] = q;
@@ -28,6 +46,7 @@ __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x,
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
+  S1_MARK(2);
   if (!last || threadIdx.x >= 32) return;
   __threadfence();
   // last block, warp 0: fixed-order sum of the per-block partials
@@ -35,6 +54,7 @@ __global__ void __launch_bounds__(256) step1_kernel(const float* __restrict__ x,
   if (threadIdx.x != 0) return;
   init_result(out, n);  // NaN-fill the record first (no separate launch): later steps fill it in
   step1_epilogue(a, q, n, K, atomicAdd(&ctrl->nonfinite, 0) != 0, out);
+  S1_MARK(3);
 }
 
 cudaError_t launch_step1(const float* x, int64_t n, Ctrl* ctrl, double* partials, plugin_result* out,
@@ -89,3 +109,9 @@ cudaError_t launch_finalize(int what, Ctrl* ctrl, int slot, const plugin_fx128* 
 }
 
 }  // namespace plg
+
+#ifdef SORT_TIMING
+extern "C" int plugin_debug_step1_timing(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, plg::g_step1_timing, sizeof(unsigned long long) * 64 * 4);
+}
+#endif

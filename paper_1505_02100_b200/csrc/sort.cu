@@ -10,6 +10,19 @@
 // digit with 8 stable 1-bit splits in shared memory).
 #include <cstdlib>
 
+// -DSORT_TIMING (tools/sort_phases.py; never in the product build): thread 0 of each block-sort
+// or merge CTA records %globaltimer at its phase boundaries into g_sort_timing (16 words per CTA)
+#ifdef SORT_TIMING
+__device__ unsigned long long g_sort_timing[64 * 16];
+#define SB_MARK(k)                                                             \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 64) {                                 \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      g_sort_timing[blockIdx.x * 16 + (k)] = t_;                               \
+    }                                                                          \
+  } while (0)
+#endif
 #include "blocksort.cuh"
 #include "common.cuh"
 
@@ -179,6 +192,7 @@ __global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict
                                                          unsigned int* __restrict__ tmp, float* __restrict__ xs) {
   __shared__ unsigned int runs[kBlockSortN];
   __shared__ unsigned int out[kBlockSortN];
+  SB_MARK(0);
   const int64_t base = (int64_t)blockIdx.x * kBlockSortN;
   unsigned int k[8];
 #pragma unroll
@@ -193,6 +207,7 @@ __global__ void __launch_bounds__(256) sort_block_kernel(const float* __restrict
   } else {
     for (int i = threadIdx.x; i < cnt; i += 256) tmp[base + i] = out[i];
   }
+  SB_MARK(7);
 }
 
 // every key of the sorted blocks to its final position: its index in its block plus, per other
@@ -201,8 +216,32 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
                                                          float* __restrict__ xs) {
   // all sorted blocks in shared memory (n <= kBlockSortMax: <= 128 KB), then shared-memory searches
   extern __shared__ unsigned int sb[];
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sb[i] = __ldg(tmp + i);
+  SB_MARK(8);
+  {
+    // 16-byte loads, up to kMergeLoads in flight per thread before the first store (one L2 round
+    // trip for n <= 16384 instead of one per 4 keys: the fill was half the kernel's time in ncu;
+    // sort + Step I 28.9 -> 22.8 us at n = 16384, 48.4 -> 37.1 at 32768, profiles/r05_prep_ab.jsonl)
+    constexpr int kMergeLoads = 16;
+    const int64_t n4 = n >> 2;  // tmp and sb are 16-byte aligned (workspace layout, dynamic smem)
+    const uint4* src4 = reinterpret_cast<const uint4*>(tmp);
+    uint4* dst4 = reinterpret_cast<uint4*>(sb);
+    for (int64_t b = threadIdx.x; b < n4; b += (int64_t)kMergeLoads * blockDim.x) {
+      uint4 v[kMergeLoads];
+#pragma unroll
+      for (int k = 0; k < kMergeLoads; ++k) {
+        const int64_t i = b + (int64_t)k * blockDim.x;
+        if (i < n4) v[k] = __ldg(src4 + i);
+      }
+#pragma unroll
+      for (int k = 0; k < kMergeLoads; ++k) {
+        const int64_t i = b + (int64_t)k * blockDim.x;
+        if (i < n4) dst4[i] = v[k];
+      }
+    }
+    for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) sb[i] = __ldg(tmp + i);
+  }
   __syncthreads();
+  SB_MARK(9);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / kBlockSortN);
     const unsigned int v = sb[i];
@@ -236,6 +275,7 @@ __global__ void __launch_bounds__(256) sort_merge_kernel(const unsigned int* __r
     }
     reinterpret_cast<unsigned int*>(xs)[rank] = key2bits(v);
   }
+  SB_MARK(10);
 }
 
 // x (float) -> xs (float, ascending).  tmp: n uint32; hist: 256*nb uint32.
@@ -294,3 +334,9 @@ cudaError_t launch_sort(const float* x, int64_t n, float* xs, unsigned int* tmp,
 }
 
 }  // namespace plg
+
+#ifdef SORT_TIMING
+extern "C" int plugin_debug_sort_timing(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_sort_timing, sizeof(unsigned long long) * 64 * 16);
+}
+#endif
