@@ -356,6 +356,10 @@ __device__ __forceinline__ double psi_tile_sum(const float* sx, const float* __r
 // CTAs or clusters (psi_small_kernel of the multi-kernel path and the single-launch cluster kernel
 // of fused.cu give the same bits).  No barrier.
 constexpr int kPsiSmallT = 64;
+#ifndef PSI_CHUNK64_UNROLL
+#define PSI_CHUNK64_UNROLL 16  // iterations of 4 columns unrolled in a full chunk (16: all)
+#endif
+constexpr int kChunk64Unroll = PSI_CHUNK64_UNROLL;
 
 __device__ __forceinline__ double row_comp(int64_t i) { return exp2(-(double)row_phase(i)); }
 
@@ -369,7 +373,7 @@ __device__ __forceinline__ Fx128 psi_chunk64(const float* cols, int jcount, floa
   const float4* c4 = reinterpret_cast<const float4*>(cols);
   u64 acc = 0ull;
   if (jcount >= kPsiSmallT) {
-#pragma unroll
+#pragma unroll(kChunk64Unroll)
     for (int q = 0; q < kPsiSmallT / 4; ++q) {
       const float4 t = LDG ? __ldg(c4 + q) : c4[q];
       pair2<ORDER, false, false, true>(pk2(t.x, t.y), xi, s2, ph, acc);
