@@ -50,11 +50,13 @@ inline int64_t psi_tile_edge(int64_t n, int r) {
 }
 inline int64_t psi_blocks(int64_t n, int r) { int64_t T = psi_tile_edge(n, r); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n, int r) { int64_t b = psi_blocks(n, r); return b * (b + 1) / 2; }
-// the pass's schedulable work items for n samples (a function of n only): whole tiles, then the
-// column quarters of the tail tiles (psi.cu); launch_psi ranges and the multi-GPU shards
-// (plugin_shard_tiles) count these.  psi_work_item: rows [out0, out1), columns [out2, out3) and
-// weight out4 of one item (host)
-constexpr int kTailSplit = 4;
+// the pass's schedulable work items for n samples (a function of n and r only): whole tiles, then
+// -- from 2000 tiles on, psi.cu -- the kTailCols-column slices of the remainder tiles; launch_psi
+// ranges and the multi-GPU shards (plugin_shard_tiles) count these.  psi_work_item: rows
+// [out0, out1), columns [out2, out3) and weight out4 of one item (host)
+constexpr int kTailCols = 64;
+constexpr int kSchedSms = 148;  // SMs of a B200: the remainder is tiles mod kSchedSms (a constant, so items depend on n only)
+int psi_sched_mode(int64_t tiles);  // 0 whole tiles, 1 remainder slices, 2 slices + per-SM quota of the whole tiles
 int64_t psi_work_units(int64_t n, int r);
 int64_t psi_tail_head(int64_t n, int r);
 bool psi_work_item(int64_t n, int r, int64_t item, int64_t* out);
@@ -80,9 +82,11 @@ struct Ctrl {                       // zeroed at the start of every API call
   long long distinct;               // number of distinct values of the sample (group.cu)
   int grouped;                      // 1: the passes run grouped by distinct value in fp64 (group.cu)
   unsigned int group_done;          // last-CTA-done counter of group_count_kernel
-  unsigned int pad[50];
+  unsigned int sm_cnt[2][kSchedSms];  // whole tiles claimed per SM and slot (scheduler mode 2, psi.cu)
+  unsigned int smq_used[2];         // a quota pass ran on the slot and its counters are not yet reset
+  unsigned int pad[4];
 };
-static_assert(sizeof(Ctrl) <= 512, "ctrl block");
+static_assert(sizeof(Ctrl) <= 2048, "ctrl block");
 
 struct Layout {
   size_t ctrl, step1, xs, tmp, hist, result, fused, grp_heads, grp_v, grp_s, total;

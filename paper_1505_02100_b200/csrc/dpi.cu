@@ -74,6 +74,10 @@ __global__ void dpi_finalize_kernel(Ctrl* ctrl, int slot, int j, plugin_dpi_resu
   ctrl->acc[slot].lo = 0ull;  // reset for the next pass on this workspace
   ctrl->acc[slot].hi = 0ll;
   ctrl->tile_counter[slot] = 0ull;
+  if (ctrl->smq_used[slot]) {  // a quota pass (psi.cu, scheduler mode 2): its per-SM counters
+    for (int k = 0; k < kSchedSms; ++k) ctrl->sm_cnt[slot][k] = 0u;
+    ctrl->smq_used[slot] = 0u;
+  }
   if (out->status != PLUGIN_OK) return;
   const int r = 2 * j + 2;
   const double nd = (double)out->n;

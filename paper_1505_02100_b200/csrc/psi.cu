@@ -94,12 +94,14 @@ template <int R, int ORDER>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, int64_t head,
-           PsiFin fin) {
+           int smq, PsiFin fin) {
   static_assert(R >= 1, "R = 0 (small tiles) runs psi_small_kernel");
+  static_assert(kPsiThreads >= kSchedSms, "the steal scan reads one per-SM counter per thread");
   constexpr int T = kPsiThreads * R;
   __shared__ __align__(16) float sx[T];
   __shared__ double red[kPsiThreads / 32];
   __shared__ long long s_tile;
+  __shared__ int s_phase, s_pick;
 
   // the sample is heavily tied: group.cu's exact pass evaluates this one (and finalises)
   if (ctrl->grouped) return;
@@ -125,23 +127,70 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   }
 #endif
 
+  // Per-SM quota (smq: scheduler mode 2, whole-range passes only): the head's whole tiles are
+  // dealt q = head / kSchedSms to each SM -- a CTA takes tile k kSchedSms + smid while its SM's
+  // counter k < q (phase 0) --, then the remainder's column slices go out by the global counter to
+  // whichever CTA is free (phase 1), and a CTA that finds the slices gone takes whole tiles left on
+  // other SMs' quotas (phase 2: SMs that host no CTA of this grid, or that run behind).  Every item
+  // is claimed exactly once whatever the placement, and the pass's sum is an exact integer, so the
+  // result does not depend on who ran what.  Without smq: items in order from the global counter.
+  unsigned int smid = 0;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const unsigned int quota = smq ? (unsigned int)(head / kSchedSms) : 0u;
+  int phase = smq ? 0 : 1;
   for (;;) {
-    if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
-    __syncthreads();
+    if (phase < 2) {
+      if (tid == 0) {
+        long long it = -1;
+        int ph = phase;
+        if (ph == 0) {
+          const unsigned int k = smid < (unsigned int)kSchedSms ? atomicAdd(&ctrl->sm_cnt[slot][smid], 1u) : quota;
+          if (k < quota) it = (long long)k * kSchedSms + (long long)smid;
+          else ph = 1;
+        }
+        if (ph == 1) {
+          const long long f = (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
+          if (!smq) it = tile_begin + f;            // past tile_end: the pass is done for this CTA
+          else if (head + f < tile_end) it = head + f;
+          else ph = 2;
+        }
+        s_tile = it;
+        s_phase = ph;
+      }
+      __syncthreads();
+      phase = s_phase;
+    }
+    if (phase == 2) {
+      // steal: find an SM whose quota is not used up (one counter per thread), try to take from it
+      if (tid == 0) s_pick = -1;
+      __syncthreads();
+      if (tid < kSchedSms && *reinterpret_cast<volatile unsigned int*>(&ctrl->sm_cnt[slot][tid]) < quota)
+        atomicMax(&s_pick, tid);
+      __syncthreads();
+      const int v = s_pick;
+      if (v < 0) break;  // every whole tile is claimed
+      if (tid == 0) {
+        const unsigned int k = atomicAdd(&ctrl->sm_cnt[slot][v], 1u);
+        s_tile = k < quota ? (long long)k * kSchedSms + v : -1;
+      }
+      __syncthreads();
+      if (s_tile < 0) continue;  // someone else took it: scan again (the scan's first barrier orders s_tile)
+    }
     const int64_t item = s_tile;
 #ifdef PSI_TIMING
     if (ntiles == 0) PT_MARK(1, gtimer());
 #endif
     if (item >= tile_end) break;
     // work item -> tile t and its column range [k0, k0 + kw): items < head are whole tiles, the
-    // rest are column quarters of the tail tiles (psi_tail_head)
+    // rest are the kTailCols-column slices of the remainder tiles (psi_tail_head)
     int64_t t = item;
     int k0 = 0, kw = T;
     if (item >= head) {
+      constexpr int kSplit = T / kTailCols;
       const int64_t qq = item - head;
-      t = head + qq / kTailSplit;
-      kw = T / kTailSplit;
-      k0 = (int)(qq % kTailSplit) * kw;
+      t = head + qq / kSplit;
+      kw = kTailCols;
+      k0 = (int)(qq % kSplit) * kTailCols;
     }
     int64_t bi, bj;
     tile_coords(t, nb, bi, bj);
@@ -207,6 +256,15 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   PT_MARK(7, ntiles);
 #endif
   psi_cta_done(cta_acc, ctrl, slot, fin, n, &last);
+  // quota counters: reset by the pass's last CTA for a later pass on the slot; without a PsiFin the
+  // 1-thread kernel that follows and takes the slot's total resets them (smq_used)
+  if (smq) {
+    if (fin.what >= 0) {
+      if (last && tid < kSchedSms) ctrl->sm_cnt[slot][tid] = 0u;
+    } else if (tid == 0 && blockIdx.x == 0) {
+      ctrl->smq_used[slot] = 1u;
+    }
+  }
 #ifdef PSI_TIMING
   PT_MARK(5, gtimer());
 #endif
@@ -269,30 +327,39 @@ static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, 
   return cudaGetLastError();
 }
 
-// resident CTAs of a B200 (148 SMs) at the occupancy the kernel is built for
-static int64_t psi_ref_slots(int R) { return 148LL * (R >= 8 ? 2 : (R <= 2 ? PSI_OCC_R12 : 3)); }
+// Work items (a function of n and r only -- and of the A/B switch PLUGIN_PSI_TAIL --, so shards and
+// any grid give the same items and bits).  With fewer than kSplitMinTiles tiles every tile is whole.
+// From kSplitMinTiles tiles on (n >= 32768) the first tiles - tiles mod kSchedSms tiles are whole
+// and the remainder tiles are cut column-wise into T / kTailCols items of kTailCols columns, which
+// the atomic counter hands to the CTAs that run ahead at the end of the pass, and the whole tiles
+// are dealt evenly to the SMs (the per-SM quota of psi_kernel): mode 2.  Measured as CUDA graphs,
+// whole tiles -> mode 2 (profiles/r07_smq.jsonl): plugin_h 327 -> 315 us at n = 32768, 1171 -> 1111
+// at 65536, 695 -> 688 at 49152, 2498 -> 2468 at 100000, 16127 -> 16003 at 262144, unchanged at
+// 131072 and config 4; below kSplitMinTiles tiles the slices lose (n = 8192: +3%, 24576: +4%) and
+// the quota alone gains 1% at n = 16384, so those sizes keep whole tiles.  PLUGIN_PSI_TAIL=0 / 1 / 2
+// forces whole tiles / slices without the quota / slices with it at any size with at least
+// kSchedSms tiles (A/B).  Earlier: slices without the quota lost 1-13% at n = 8192-24576
+// (profiles/r05_ab_tail_slices.jsonl); column quarters of the last S + tiles mod S tiles were 7-11%
+// slower at n = 8K-25K (profiles/r02o_ab_tail.jsonl).
+constexpr int64_t kSplitMinTiles = 2000;
+int psi_sched_mode(int64_t tiles) {
+  if (tiles < kSchedSms) return 0;
+  const char* e = getenv("PLUGIN_PSI_TAIL");
+  if (e && e[0] >= '0' && e[0] <= '2' && e[1] == 0) return e[0] - '0';
+  return tiles >= kSplitMinTiles ? 2 : 0;
+}
 
-// Tail split (A/B option, off by default): the last S + (tiles mod S) tiles (S = resident CTAs
-// of a B200) cut into kTailSplit column quarters so a pass would end on fine items.  Measured
-// (profiles/r02o_ab_tail.jsonl, CUDA graphs): 7-11% slower at n = 8K..25K (the per-item setup of
-// 4x more items outweighs the shorter tail), +3% at 64K, within 1% from 128K; so items are whole
-// tiles unless PLUGIN_PSI_TAIL=1.  A function of n (and that switch) only.  Items [0, head) are
-// whole tiles.
 int64_t psi_tail_head(int64_t n, int r) {
   const int64_t tiles = psi_tiles(n, r);
   const int R = psi_rows_per_thread(n, r);
-  if (R == 0) return tiles;
-  const char* e = getenv("PLUGIN_PSI_TAIL");
-  if (!e || e[0] != '1') return tiles;
-  const int64_t S = psi_ref_slots(R);
-  const int64_t tail = S + tiles % S;
-  return tiles > tail ? tiles - tail : 0;
+  if (R == 0 || psi_sched_mode(tiles) == 0) return tiles;
+  return tiles - tiles % kSchedSms;
 }
 
 int64_t psi_work_units(int64_t n, int r) {
   if (n <= 0) return 0;
   const int64_t tiles = psi_tiles(n, r), head = psi_tail_head(n, r);
-  return head + kTailSplit * (tiles - head);
+  return head + (psi_tile_edge(n, r) / kTailCols) * (tiles - head);
 }
 
 bool psi_work_item(int64_t n, int r, int64_t item, int64_t* out) {
@@ -300,9 +367,10 @@ bool psi_work_item(int64_t n, int r, int64_t item, int64_t* out) {
   const int64_t T = psi_tile_edge(n, r), nb = (n + T - 1) / T, head = psi_tail_head(n, r);
   int64_t t = item, k0 = 0, kw = T;
   if (item >= head) {
-    t = head + (item - head) / kTailSplit;
-    kw = T / kTailSplit;
-    k0 = ((item - head) % kTailSplit) * kw;
+    const int64_t split = T / kTailCols;
+    t = head + (item - head) / split;
+    kw = kTailCols;
+    k0 = ((item - head) % split) * kw;
   }
   // row-major upper block triangle incl. the diagonal (as tile_coords)
   int64_t b = 0;
@@ -352,8 +420,11 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   int64_t tiles = te - tb;
   int grid = (int)(tiles < grid_cap ? tiles : grid_cap);
   if (grid < 1) grid = 1;
-  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te,
-                                                   psi_tail_head(n, ORDER), fin);
+  // the per-SM quota needs the whole item range in one grid
+  const int64_t head = psi_tail_head(n, ORDER);
+  const int smq = psi_sched_mode(psi_tiles(n, ORDER)) == 2 && tb == 0 && te == psi_work_units(n, ORDER) && head >= kSchedSms && head < te;
+  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, head, smq,
+                                                   fin);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,10 @@ __global__ void finalize_kernel(int what, Ctrl* ctrl, int slot, const plugin_fx1
     ctrl->acc[slot].lo = 0ull;
     ctrl->acc[slot].hi = 0ll;
     ctrl->tile_counter[slot] = 0ull;
+    if (ctrl->smq_used[slot]) {  // a quota pass (psi.cu, scheduler mode 2): its per-SM counters
+      for (int k = 0; k < kSchedSms; ++k) ctrl->sm_cnt[slot][k] = 0u;
+      ctrl->smq_used[slot] = 0u;
+    }
   }
   if (total) acc = limbs_to_fx(total);
   if (n <= 0 && out) n = out->n;

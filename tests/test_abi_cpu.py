@@ -77,9 +77,16 @@ def test_rows_per_thread_by_order(L):
     assert L.plugin_tile_edge(1000, 6) == L.plugin_tile_edge(1000, 4) == 64
 
 
+@pytest.mark.parametrize("mode", ["", "1", "2"])
 @pytest.mark.parametrize("n", [1, 2, 2048, 2049, 5000, 16384, 50000, 131072, 1 << 20])
-def test_work_items_partition_the_triangle(n):
-    # every tile's columns are covered exactly once by its items (whole, or 4 quarters), rows
+def test_work_items_partition_the_triangle(n, mode, monkeypatch):
+    # mode: the scheduler A/B switch PLUGIN_PSI_TAIL (1, 2: the last tiles mod 148 tiles as 64-column
+    # slices) -- the item definitions are read from the environment at every call
+    if mode:
+        monkeypatch.setenv("PLUGIN_PSI_TAIL", mode)
+    else:
+        monkeypatch.delenv("PLUGIN_PSI_TAIL", raising=False)
+    # every tile's columns are covered exactly once by its items (whole, or column slices), rows
     # and weights are the tile's; the items cover exactly the upper block triangle
     from paper_1505_02100_b200 import plugin as P
     order = 6 if n % 2 else 4
@@ -93,7 +100,7 @@ def test_work_items_partition_the_triangle(n):
         bi, bj = r0 // T, (c0 // T) if c1 > c0 else None
         assert r0 == bi * T and r1 == min(n, r0 + T) and 0 <= r0 < r1 <= n
         if bj is None:
-            continue                       # a quarter past the sample's end: no pairs
+            continue                       # a slice past the sample's end: no pairs
         assert bj >= bi and w == (1 if bi == bj else 2) and c1 <= min(n, bj * T + T)
         cover.setdefault((bi, bj), []).append((c0, c1))
     if step == 1:
@@ -103,7 +110,7 @@ def test_work_items_partition_the_triangle(n):
         full = [(bj * T, min(n, bj * T + T))]
         if len(spans) == 1 or spans[0][1] - spans[0][0] == full[0][1] - full[0][0]:
             assert spans == full or len(spans) == 1
-        else:                              # quarters: contiguous, disjoint, ending at the block's end
+        else:                              # slices: contiguous, disjoint, ending at the block's end
             for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
                 assert a1 == b0
             assert spans[0][0] == full[0][0] and spans[-1][1] == full[0][1]

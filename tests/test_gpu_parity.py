@@ -257,7 +257,7 @@ def test_full_size_sampled_tile_shards(P, oracle_mod, k):
             got = from_limbs(part.cpu().tolist()) / 2.0 ** 64 * phi0
             ib, ie = P.plugin_shard_tiles(n, r, rank, world)
             ref = 0.0
-            for it in range(ib, ie):        # each work item: a tile or a tail-tile quarter
+            for it in range(ib, ie):        # each work item: a tile or a column slice of a remainder tile
                 rows, cols, w = P.plugin_work_item(n, r, it)
                 if cols[1] > cols[0]:
                     ref += w * oracle_mod.psi_block_sum(zs, g, r, *rows, *cols)
@@ -602,6 +602,30 @@ def _one_tile(P, n, r, t, ntiles, dres, ws):
     return from_limbs(part.cpu().tolist()) / 2.0 ** 64 / math.sqrt(2 * math.pi)
 
 
+def _tile_of_item(P, n, r, item, ntiles):
+    """All work items of the tile that holds `item`: the item itself when tiles are whole (the
+    default), the tile's column slices under the scheduler A/B switch PLUGIN_PSI_TAIL."""
+    T = P.plugin_tile_edge(n, r)
+
+    def key(it):
+        rows, cols, _ = P.plugin_work_item(n, r, it)
+        return rows[0], cols[0] // T
+
+    k, lo, hi = key(item), item, item + 1
+    while lo > 0 and key(lo - 1) == k:
+        lo -= 1
+    while hi < ntiles and key(hi) == k:
+        hi += 1
+    return range(lo, hi)
+
+
+def _tile_got_ref(P, oracle_mod, zs, g, r, n, item, ntiles, dres, ws):
+    """GPU and oracle sums over the whole tile that holds `item` (one psi_r_shard call per item)."""
+    items = _tile_of_item(P, n, r, item, ntiles)
+    return (sum(_one_tile(P, n, r, t, ntiles, dres, ws) for t in items),
+            sum(_tile_sum_oracle(oracle_mod, P, zs, g, r, n, t) for t in items))
+
+
 def _bandwidth_record(P, n, g_a, g_b):
     res = P.plugin_result()
     res.status, res.n, res.g1, res.g2 = 0, n, g_a, g_b
@@ -631,8 +655,7 @@ def test_wide_tiles_with_outliers_at_full_size(P, oracle_mod, n):
                         (nb - 2) * nb - (nb - 2) * (nb - 3) // 2 + 1})                    # row nb-2, last column
         dres = _bandwidth_record(P, n, g, g)
         for t in picks:
-            got = _one_tile(P, n, r, t, ntiles, dres, ws)
-            ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
+            got, ref = _tile_got_ref(P, oracle_mod, zs, g, r, n, t, ntiles, dres, ws)
             assert math.isfinite(got)
             # relative 1e-5; terms below the fp32 range (e^(-u^2/2) < 2^-126: the far tiles) are
             # +0 on the GPU, so an absolute T^2 2^-100 is allowed on top
@@ -655,8 +678,7 @@ def test_general_r_pass_at_cfg4_sampled_tiles(P, oracle_mod, r):
     nb = -(-n // T)
     dres = _bandwidth_record(P, n, g, g)
     for t in (0, 5, nb + 3, ntiles // 2, ntiles // 2 + 1, ntiles - 3, ntiles - 1):
-        got = _one_tile(P, n, r, t, ntiles, dres, ws)
-        ref = _tile_sum_oracle(oracle_mod, P, zs, g, r, n, t)
+        got, ref = _tile_got_ref(P, oracle_mod, zs, g, r, n, t, ntiles, dres, ws)
         assert abs(got - ref) <= TOL * abs(ref) + T * T * 2.0 ** -100, (r, t, P.plugin_work_item(n, r, t), got, ref)
 
 

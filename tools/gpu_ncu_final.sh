@@ -7,5 +7,5 @@ timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 CMD2="python bench.py --steps 1 --warmup 0 --no-cpu-baseline"
 timeout 300 $CMD2 > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:psi_kernel -s 0 -c 2 -o gpurun_out/prof $CMD2 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:^psi_kernel -s 0 -c 2 -o gpurun_out/prof $CMD2 > gpurun_out/ncu_full.log 2>&1
 echo done
