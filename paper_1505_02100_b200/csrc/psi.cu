@@ -90,11 +90,11 @@ __device__ __forceinline__ void psi_cta_done(Fx128 cta_acc, Ctrl* ctrl, int slot
 template <int R>
 struct PsiOcc { static constexpr int value = (R >= 8) ? 2 : (R <= 2 ? PSI_OCC_R12 : 3); };
 
-template <int R, int ORDER>
+template <int R, int ORDER, bool SMQ>
 __global__ void __launch_bounds__(kPsiThreads, PsiOcc<R>::value)
 psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, const double* g_dev,
            const int32_t* status_dev, Ctrl* ctrl, int slot, int64_t tile_begin, int64_t tile_end, int64_t head,
-           int smq, PsiFin fin) {
+           unsigned int quota, PsiFin fin) {
   static_assert(R >= 1, "R = 0 (small tiles) runs psi_small_kernel");
   static_assert(kPsiThreads >= kSchedSms, "the steal scan reads one per-SM counter per thread");
   constexpr int T = kPsiThreads * R;
@@ -127,54 +127,58 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   }
 #endif
 
-  // Per-SM quota (smq: scheduler mode 2, whole-range passes only): the head's whole tiles are
-  // dealt q = head / kSchedSms to each SM -- a CTA takes tile k kSchedSms + smid while its SM's
-  // counter k < q (phase 0) --, then the remainder's column slices go out by the global counter to
-  // whichever CTA is free (phase 1), and a CTA that finds the slices gone takes whole tiles left on
-  // other SMs' quotas (phase 2: SMs that host no CTA of this grid, or that run behind).  Every item
-  // is claimed exactly once whatever the placement, and the pass's sum is an exact integer, so the
-  // result does not depend on who ran what.  Without smq: items in order from the global counter.
-  unsigned int smid = 0;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-  const unsigned int quota = smq ? (unsigned int)(head / kSchedSms) : 0u;
-  int phase = smq ? 0 : 1;
+  // Per-SM quota (SMQ: scheduler mode 2, whole-range passes only; its own instantiation, so the
+  // other passes' code is untouched): the head's whole tiles are dealt quota = head / kSchedSms to
+  // each SM -- a CTA takes tile k kSchedSms + smid while its SM's counter k < quota (phase 0) --,
+  // then the remainder's column slices go out by the global counter to whichever CTA is free
+  // (phase 1), and a CTA that finds the slices gone takes whole tiles left on other SMs' quotas
+  // (phase 2: SMs that host no CTA of this grid, or that run behind).  Every item is claimed exactly
+  // once whatever the placement, and the pass's sum is an exact integer, so the result does not
+  // depend on who ran what.  Without SMQ: items in order from the global counter.
+  int phase = 0;
   for (;;) {
-    if (phase < 2) {
-      if (tid == 0) {
-        long long it = -1;
-        int ph = phase;
-        if (ph == 0) {
-          const unsigned int k = smid < (unsigned int)kSchedSms ? atomicAdd(&ctrl->sm_cnt[slot][smid], 1u) : quota;
-          if (k < quota) it = (long long)k * kSchedSms + (long long)smid;
-          else ph = 1;
+    if constexpr (!SMQ) {
+      if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
+      __syncthreads();
+    } else {
+      if (phase < 2) {
+        if (tid == 0) {
+          long long it = -1;
+          int ph = phase;
+          if (ph == 0) {
+            unsigned int smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const unsigned int k = smid < (unsigned int)kSchedSms ? atomicAdd(&ctrl->sm_cnt[slot][smid], 1u) : quota;
+            if (k < quota) it = (long long)k * kSchedSms + (long long)smid;
+            else ph = 1;
+          }
+          if (ph == 1) {
+            const long long f = (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
+            if (head + f < tile_end) it = head + f;
+            else ph = 2;
+          }
+          s_tile = it;
+          s_phase = ph;
         }
-        if (ph == 1) {
-          const long long f = (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
-          if (!smq) it = tile_begin + f;            // past tile_end: the pass is done for this CTA
-          else if (head + f < tile_end) it = head + f;
-          else ph = 2;
+        __syncthreads();
+        phase = s_phase;
+      }
+      if (phase == 2) {
+        // steal: find an SM whose quota is not used up (one counter per thread), try to take from it
+        if (tid == 0) s_pick = -1;
+        __syncthreads();
+        if (tid < kSchedSms && *reinterpret_cast<volatile unsigned int*>(&ctrl->sm_cnt[slot][tid]) < quota)
+          atomicMax(&s_pick, tid);
+        __syncthreads();
+        const int v = s_pick;
+        if (v < 0) break;  // every whole tile is claimed
+        if (tid == 0) {
+          const unsigned int k = atomicAdd(&ctrl->sm_cnt[slot][v], 1u);
+          s_tile = k < quota ? (long long)k * kSchedSms + v : -1;
         }
-        s_tile = it;
-        s_phase = ph;
+        __syncthreads();
+        if (s_tile < 0) continue;  // someone else took it: scan again (the scan's first barrier orders s_tile)
       }
-      __syncthreads();
-      phase = s_phase;
-    }
-    if (phase == 2) {
-      // steal: find an SM whose quota is not used up (one counter per thread), try to take from it
-      if (tid == 0) s_pick = -1;
-      __syncthreads();
-      if (tid < kSchedSms && *reinterpret_cast<volatile unsigned int*>(&ctrl->sm_cnt[slot][tid]) < quota)
-        atomicMax(&s_pick, tid);
-      __syncthreads();
-      const int v = s_pick;
-      if (v < 0) break;  // every whole tile is claimed
-      if (tid == 0) {
-        const unsigned int k = atomicAdd(&ctrl->sm_cnt[slot][v], 1u);
-        s_tile = k < quota ? (long long)k * kSchedSms + v : -1;
-      }
-      __syncthreads();
-      if (s_tile < 0) continue;  // someone else took it: scan again (the scan's first barrier orders s_tile)
     }
     const int64_t item = s_tile;
 #ifdef PSI_TIMING
@@ -258,7 +262,7 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   psi_cta_done(cta_acc, ctrl, slot, fin, n, &last);
   // quota counters: reset by the pass's last CTA for a later pass on the slot; without a PsiFin the
   // 1-thread kernel that follows and takes the slot's total resets them (smq_used)
-  if (smq) {
+  if constexpr (SMQ) {
     if (fin.what >= 0) {
       if (last && tid < kSchedSms) ctrl->sm_cnt[slot][tid] = 0u;
     } else if (tid == 0 && blockIdx.x == 0) {
@@ -329,7 +333,7 @@ static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, 
 
 // Work items (a function of n and r only -- and of the A/B switch PLUGIN_PSI_TAIL --, so shards and
 // any grid give the same items and bits).  With fewer than kSplitMinTiles tiles every tile is whole.
-// From kSplitMinTiles tiles on (n >= 32768) the first tiles - tiles mod kSchedSms tiles are whole
+// From kSplitMinTiles to kSplitMaxTiles tiles (n = 32768 to ~290000 for r >= 6, to ~580000 for r <= 4) the first tiles - tiles mod kSchedSms tiles are whole
 // and the remainder tiles are cut column-wise into T / kTailCols items of kTailCols columns, which
 // the atomic counter hands to the CTAs that run ahead at the end of the pass, and the whole tiles
 // are dealt evenly to the SMs (the per-SM quota of psi_kernel): mode 2.  Measured as CUDA graphs,
@@ -341,12 +345,15 @@ static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, 
 // kSchedSms tiles (A/B).  Earlier: slices without the quota lost 1-13% at n = 8192-24576
 // (profiles/r05_ab_tail_slices.jsonl); column quarters of the last S + tiles mod S tiles were 7-11%
 // slower at n = 8K-25K (profiles/r02o_ab_tail.jsonl).
-constexpr int64_t kSplitMinTiles = 2000;
+// Above kSplitMaxTiles tiles (configs 4 and 5) the pass is hundreds of waves long, the
+// slices measured no gain, and whole tiles keep the multi-GPU shards (equal item counts) equal in
+// work -- sliced remainders would leave the last rank short by tiles mod 148 tiles.
+constexpr int64_t kSplitMinTiles = 2000, kSplitMaxTiles = 40000;
 int psi_sched_mode(int64_t tiles) {
   if (tiles < kSchedSms) return 0;
   const char* e = getenv("PLUGIN_PSI_TAIL");
   if (e && e[0] >= '0' && e[0] <= '2' && e[1] == 0) return e[0] - '0';
-  return tiles >= kSplitMinTiles ? 2 : 0;
+  return (tiles >= kSplitMinTiles && tiles <= kSplitMaxTiles) ? 2 : 0;
 }
 
 int64_t psi_tail_head(int64_t n, int r) {
@@ -414,7 +421,7 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   static DevCache cap_cache;
   const int grid_cap = dev_cached(cap_cache, [](int dev) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_kernel<R, ORDER>, kPsiThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, psi_kernel<R, ORDER, false>, kPsiThreads, 0);
     return device_sms(dev) * (occ > 0 ? occ : 1);
   });
   int64_t tiles = te - tb;
@@ -422,9 +429,14 @@ static cudaError_t launch_t(const float* xs, int64_t n, int skip, double g, cons
   if (grid < 1) grid = 1;
   // the per-SM quota needs the whole item range in one grid
   const int64_t head = psi_tail_head(n, ORDER);
-  const int smq = psi_sched_mode(psi_tiles(n, ORDER)) == 2 && tb == 0 && te == psi_work_units(n, ORDER) && head >= kSchedSms && head < te;
-  psi_kernel<R, ORDER><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, head, smq,
-                                                   fin);
+  const bool smq = psi_sched_mode(psi_tiles(n, ORDER)) == 2 && tb == 0 && te == psi_work_units(n, ORDER) &&
+                   head >= kSchedSms && head < te;
+  if (smq)
+    psi_kernel<R, ORDER, true><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, head,
+                                                           (unsigned int)(head / kSchedSms), fin);
+  else
+    psi_kernel<R, ORDER, false><<<grid, kPsiThreads, 0, s>>>(xs, n, skip, g, g_dev, status_dev, ctrl, slot, tb, te, head,
+                                                            0u, fin);
   return cudaGetLastError();
 }
 

@@ -194,6 +194,51 @@ def test_shards_sum_to_single_gpu_bit_exact(P, world):
         assert r[k] == ref[k], (k, r[k], ref[k])
 
 
+@pytest.mark.parametrize("n", [4400, 16384, 40000, 70000])
+def test_scheduler_modes_same_result_and_shards_bit_exact(P, n, monkeypatch):
+    """The pass scheduler (psi.cu): whole tiles from one counter (PLUGIN_PSI_TAIL=0), the remainder
+    tiles as 64-column slices (1), slices plus the per-SM quota of the whole tiles (2; the default
+    from 2000 tiles).  In every mode the result is reproducible bit for bit, the shards of 3 ranks sum
+    to plugin_h's bits (the items depend on n only), and the modes agree to fp64 rounding (the same
+    fp32 pair terms, grouped into different items)."""
+    xh = inputs.mixture(n, 4100 + n)
+    x = torch.from_numpy(xh).cuda()
+    ws = P.workspace(n)
+    res = {}
+    for mode in ("0", "1", "2", None):
+        if mode is None:
+            monkeypatch.delenv("PLUGIN_PSI_TAIL", raising=False)
+        else:
+            monkeypatch.setenv("PLUGIN_PSI_TAIL", mode)
+        a, b = P.plugin_h_sync(x), P.plugin_h_sync(x)
+        assert a["status"] == 0 and _same(a, b), mode
+        out = P.new_result()
+        P.plugin_step1(x, out, ws)
+        for r, after in ((6, P.plugin_after_psi6), (4, P.plugin_after_psi4)):
+            tot = torch.zeros(4, dtype=torch.int64, device="cuda")
+            covered = 0
+            for rank in range(3):
+                part = P.new_partial()
+                P.psi_r_shard(n, r, rank, 3, out, part, ws)
+                tot += part
+                ib, ie = P.plugin_shard_tiles(n, r, rank, 3)
+                covered += ie - ib
+            assert covered == P.plugin_num_tiles(n, r)
+            after(tot, out)
+        sh = P.read_result(out)
+        for k in ("psi6", "g2", "psi4", "h"):
+            assert sh[k] == a[k], (mode, k, sh[k], a[k])
+        res[mode] = a
+    T, tiles = P.plugin_tile_edge(n, 6), P.plugin_num_tiles(n, 6)        # (default mode again)
+    nb = -(-n // T)
+    whole = nb * (nb + 1) // 2
+    assert (tiles > whole) == (2000 <= whole <= 40000)                   # slices by default only there
+    assert _same(res[None], res["2" if tiles > whole else "0"])
+    for mode in ("1", "2"):
+        for k in ("psi6", "psi4", "h"):
+            assert rel(res[mode][k], res["0"][k]) < 1e-12, (mode, k)
+
+
 def test_data_errors(P):
     r = P.plugin_h_sync(torch.tensor([1.0, float("nan"), 2.0], device="cuda"))
     assert r["status"] == P.PLUGIN_E_NONFINITE and math.isnan(r["h"])
