@@ -195,10 +195,10 @@ plugin_status plugin_after_psi4(const plugin_fx128* d_total, plugin_result* d_ou
  * only: T x T tiles of the sorted sample's upper block triangle
  * (T = plugin_tile_edge(n, r): 64 for n <= 2048, else 256 R with R the rows per thread, which
  * depends on r: the r >= 6 passes use R <= 4); diagonal tiles are full squares, weight 1;
- * off-diagonal weight 2.  With 2000 to 40000 tiles (n = 32768 to ~290000 for r >= 6, to ~580000 for r <= 4) the last tiles mod 148
- * tiles are split column-wise into items of 64 columns, so that a pass ends on fine items (the A/B
- * switch PLUGIN_PSI_TAIL=0 keeps every tile whole; 1 and 2 split from 148 tiles on).  plugin_num_tiles:
- * the number of items;
+ * off-diagonal weight 2.  With 2000 to 5000 tiles (n ~ 32K-50K and 64.5K-101K) the last
+ * tiles mod 148 tiles are split column-wise into items of 64 columns, so that a pass ends on fine
+ * items (the A/B switch PLUGIN_PSI_TAIL=0 keeps every tile whole; 1 and 2 split from 148 tiles on).
+ * plugin_num_tiles: the number of items;
  * plugin_shard_tiles: the item range [begin, end) that `rank` of `world` owns (what
  * psi_r_shard / psi_r_shard_g process for that r, balanced to one item; an empty range for a
  * bad rank, world or r); plugin_work_item: the pairs of one item, out5 = {row begin, row end,

@@ -51,7 +51,7 @@ inline int64_t psi_tile_edge(int64_t n, int r) {
 inline int64_t psi_blocks(int64_t n, int r) { int64_t T = psi_tile_edge(n, r); return (n + T - 1) / T; }
 inline int64_t psi_tiles(int64_t n, int r) { int64_t b = psi_blocks(n, r); return b * (b + 1) / 2; }
 // the pass's schedulable work items for n samples (a function of n and r only): whole tiles, then
-// -- with 2000 to 40000 tiles, psi.cu -- the kTailCols-column slices of the remainder tiles; launch_psi
+// -- with 2000 to 5000 tiles, psi.cu -- the kTailCols-column slices of the remainder tiles; launch_psi
 // ranges and the multi-GPU shards (plugin_shard_tiles) count these.  psi_work_item: rows
 // [out0, out1), columns [out2, out3) and weight out4 of one item (host)
 constexpr int kTailCols = 64;

@@ -332,23 +332,23 @@ static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, 
 }
 
 // Work items (a function of n and r only -- and of the A/B switch PLUGIN_PSI_TAIL --, so shards and
-// any grid give the same items and bits).  With fewer than kSplitMinTiles tiles every tile is whole.
-// From kSplitMinTiles to kSplitMaxTiles tiles (n = 32768 to ~290000 for r >= 6, to ~580000 for r <= 4) the first tiles - tiles mod kSchedSms tiles are whole
-// and the remainder tiles are cut column-wise into T / kTailCols items of kTailCols columns, which
-// the atomic counter hands to the CTAs that run ahead at the end of the pass, and the whole tiles
-// are dealt evenly to the SMs (the per-SM quota of psi_kernel): mode 2.  Measured as CUDA graphs,
-// whole tiles -> mode 2 (profiles/r07_smq.jsonl): plugin_h 327 -> 315 us at n = 32768, 1171 -> 1111
-// at 65536, 695 -> 688 at 49152, 2498 -> 2468 at 100000, 16127 -> 16003 at 262144, unchanged at
-// 131072 and config 4; below kSplitMinTiles tiles the slices lose (n = 8192: +3%, 24576: +4%) and
-// the quota alone gains 1% at n = 16384, so those sizes keep whole tiles.  PLUGIN_PSI_TAIL=0 / 1 / 2
-// forces whole tiles / slices without the quota / slices with it at any size with at least
-// kSchedSms tiles (A/B).  Earlier: slices without the quota lost 1-13% at n = 8192-24576
-// (profiles/r05_ab_tail_slices.jsonl); column quarters of the last S + tiles mod S tiles were 7-11%
-// slower at n = 8K-25K (profiles/r02o_ab_tail.jsonl).
-// Above kSplitMaxTiles tiles (configs 4 and 5) the pass is hundreds of waves long, the
-// slices measured no gain, and whole tiles keep the multi-GPU shards (equal item counts) equal in
-// work -- sliced remainders would leave the last rank short by tiles mod 148 tiles.
-constexpr int64_t kSplitMinTiles = 2000, kSplitMaxTiles = 40000;
+// any grid give the same items and bits).  Outside kSplitMinTiles ... kSplitMaxTiles tiles every tile
+// is whole.  Inside (n ~ 32K-50K and 64.5K-101K: a pass of 3 to 11 waves of resident CTAs, where the
+// last wave's whole tiles cost most) the first tiles - tiles mod kSchedSms tiles are whole and the
+// remainder tiles are cut column-wise into T / kTailCols items of kTailCols columns, which the
+// atomic counter hands to the CTAs that run ahead at the end of the pass, and the whole tiles are
+// dealt evenly to the SMs (the per-SM quota of psi_kernel<.., SMQ = true>): mode 2.  Measured as
+// CUDA graphs, whole tiles -> mode 2 (profiles/r09_psi_graph_ab.jsonl): plugin_h 324.8 -> 316.5 us
+// at n = 32768, 1157 -> 1109 at 65536, 2481 -> 2444 at 100000; with more tiles the quota
+// instantiation's slightly slower tile loop outweighs the shorter tail (+0.8% at n = 49152 with
+// 4656 tiles of T = 512, +1.4% at 131072, +0.7% at 262144), and at configs 4 and 5 whole tiles
+// also keep the multi-GPU shards (equal item counts) equal in work; with fewer tiles the slices
+// lose (n = 8192: +3%, 24576: +4%, profiles/r07_smq.jsonl) and the quota alone gains 1% at
+// n = 16384.  PLUGIN_PSI_TAIL=0 / 1 / 2 forces whole tiles / slices without the quota / slices
+// with it at any size with at least kSchedSms tiles (A/B).  Earlier: slices without the quota lost
+// 1-13% at n = 8192-24576 (profiles/r05_ab_tail_slices.jsonl); column quarters of the last
+// S + tiles mod S tiles were 7-11% slower at n = 8K-25K (profiles/r02o_ab_tail.jsonl).
+constexpr int64_t kSplitMinTiles = 2000, kSplitMaxTiles = 5000;
 int psi_sched_mode(int64_t tiles) {
   if (tiles < kSchedSms) return 0;
   const char* e = getenv("PLUGIN_PSI_TAIL");

@@ -198,7 +198,7 @@ def test_shards_sum_to_single_gpu_bit_exact(P, world):
 def test_scheduler_modes_same_result_and_shards_bit_exact(P, n, monkeypatch):
     """The pass scheduler (psi.cu): whole tiles from one counter (PLUGIN_PSI_TAIL=0), the remainder
     tiles as 64-column slices (1), slices plus the per-SM quota of the whole tiles (2; the default
-    from 2000 tiles).  In every mode the result is reproducible bit for bit, the shards of 3 ranks sum
+    with 2000 to 5000 tiles).  In every mode the result is reproducible bit for bit, the shards of 3 ranks sum
     to plugin_h's bits (the items depend on n only), and the modes agree to fp64 rounding (the same
     fp32 pair terms, grouped into different items)."""
     xh = inputs.mixture(n, 4100 + n)
@@ -232,7 +232,7 @@ def test_scheduler_modes_same_result_and_shards_bit_exact(P, n, monkeypatch):
     T, tiles = P.plugin_tile_edge(n, 6), P.plugin_num_tiles(n, 6)        # (default mode again)
     nb = -(-n // T)
     whole = nb * (nb + 1) // 2
-    assert (tiles > whole) == (2000 <= whole <= 40000)                   # slices by default only there
+    assert (tiles > whole) == (2000 <= whole <= 5000)                     # slices by default only there
     assert _same(res[None], res["2" if tiles > whole else "0"])
     for mode in ("1", "2"):
         for k in ("psi6", "psi4", "h"):
