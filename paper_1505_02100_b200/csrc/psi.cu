@@ -135,12 +135,25 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   // (phase 2: SMs that host no CTA of this grid, or that run behind).  Every item is claimed exactly
   // once whatever the placement, and the pass's sum is an exact integer, so the result does not
   // depend on who ran what.  Without SMQ: items in order from the global counter.
+  // -DPSI_SMQ_SHARED_PHASE (A/B): the phase is kept in shared memory instead of a register that
+  // lives across the tile loop (one more barrier per item)
+#ifdef PSI_SMQ_SHARED_PHASE
+  if constexpr (SMQ) {
+    if (tid == 0) s_phase = 0;
+    __syncthreads();
+  }
+#else
   int phase = 0;
+#endif
   for (;;) {
     if constexpr (!SMQ) {
       if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
       __syncthreads();
     } else {
+#ifdef PSI_SMQ_SHARED_PHASE
+      int phase = s_phase;  // written by thread 0 only, between the next two barriers
+      __syncthreads();
+#endif
       if (phase < 2) {
         if (tid == 0) {
           long long it = -1;
