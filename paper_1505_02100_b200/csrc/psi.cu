@@ -135,25 +135,12 @@ psi_kernel(const float* __restrict__ xs, int64_t n, int skip, double g_host, con
   // (phase 2: SMs that host no CTA of this grid, or that run behind).  Every item is claimed exactly
   // once whatever the placement, and the pass's sum is an exact integer, so the result does not
   // depend on who ran what.  Without SMQ: items in order from the global counter.
-  // -DPSI_SMQ_SHARED_PHASE (A/B): the phase is kept in shared memory instead of a register that
-  // lives across the tile loop (one more barrier per item)
-#ifdef PSI_SMQ_SHARED_PHASE
-  if constexpr (SMQ) {
-    if (tid == 0) s_phase = 0;
-    __syncthreads();
-  }
-#else
   int phase = 0;
-#endif
   for (;;) {
     if constexpr (!SMQ) {
       if (tid == 0) s_tile = tile_begin + (long long)atomicAdd(&ctrl->tile_counter[slot], 1ull);
       __syncthreads();
     } else {
-#ifdef PSI_SMQ_SHARED_PHASE
-      int phase = s_phase;  // written by thread 0 only, between the next two barriers
-      __syncthreads();
-#endif
       if (phase < 2) {
         if (tid == 0) {
           long long it = -1;
@@ -353,7 +340,7 @@ static cudaError_t launch_small(const float* xs, int64_t n, int skip, double g, 
 // dealt evenly to the SMs (the per-SM quota of psi_kernel<.., SMQ = true>): mode 2.  Measured as
 // CUDA graphs, whole tiles -> mode 2 (profiles/r09_psi_graph_ab.jsonl): plugin_h 324.8 -> 316.5 us
 // at n = 32768, 1157 -> 1109 at 65536, 2481 -> 2444 at 100000; with more tiles the quota
-// instantiation's slightly slower tile loop outweighs the shorter tail (+0.8% at n = 49152 with
+// scheduler (its latency-bound 64-column slices) costs more than the shorter tail gains (+0.8% at n = 49152 with
 // 4656 tiles of T = 512, +1.4% at 131072, +0.7% at 262144), and at configs 4 and 5 whole tiles
 // also keep the multi-GPU shards (equal item counts) equal in work; with fewer tiles the slices
 // lose (n = 8192: +3%, 24576: +4%, profiles/r07_smq.jsonl) and the quota alone gains 1% at
